@@ -1,0 +1,80 @@
+/*
+ * mimw_b200.h — C-ABI of the B200-native hot path (libmimw_b200.so).
+ *
+ * Drop-in boundary for the reference's operator API, the pure oracle
+ * functions of /root/reference/proj/core/include/mimw/oracles.hpp (which
+ * the corpus driver tools/mimw.cpp:205-259 and the tests call through
+ * run_oracle, oracles.cpp:147-201).  Two families of entry points:
+ *
+ *   mimw_b200_oracle_*   HOST f32 buffers, exactly the reference's Tile
+ *                        semantics (row-major, shapes as in oracles.hpp);
+ *                        copies in, runs the sm_100a kernels, copies out.
+ *                        These replace the reference functions one for one.
+ *   mimw_b200_*          DEVICE buffers + a cudaStream_t (as void*), the
+ *                        production path (bf16 / e4m3 operands in HBM).
+ *
+ * Conventions: plain pointers and int64 sizes, no exceptions
+ * cross the ABI, every call returns a status code; the message of the last
+ * failure on the calling thread is available from mimw_b200_last_error().
+ * Calls are reentrant per stream.  There is no CPU fallback: without a
+ * B200 (sm_100a) device every compute entry point returns MIMW_ERR_CUDA.
+ */
+#ifndef MIMW_B200_H
+#define MIMW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MIMW_OK 0
+#define MIMW_ERR_SHAPE 1       /* dot conformance, proj/core/src/validate.cpp:314-338 */
+#define MIMW_ERR_UNSUPPORTED 2 /* dtype / layout / alignment not supported */
+#define MIMW_ERR_CUDA 3        /* CUDA runtime / launch failure, or no sm_100 device */
+#define MIMW_ERR_ARG 4         /* null pointer or bad enum */
+
+/* element types */
+#define MIMW_F32 0
+#define MIMW_BF16 1
+
+/* B operand layout */
+#define MIMW_B_KN 0 /* B[K, N] row-major — the reference's layout (oracles.cpp:21-22) */
+#define MIMW_B_NK 1 /* B[N, K] row-major (K-contiguous, "NT" GEMM) */
+
+/* precision of the host f32 entry points */
+#define MIMW_PREC_BF16 0          /* inputs rounded to bf16 (RNE), fp32 accumulate */
+#define MIMW_PREC_F32_BF16X3 1    /* split-bf16 x3 on tensor cores: ~1e-6 rel-err,
+                                     meets the reference's own 1e-4 GEMM cases */
+
+int mimw_b200_version(void);
+const char *mimw_b200_last_error(void);
+
+/* ---- GEMM:  C[M,N] = A[M,K] . B  (fp32 accumulate in TMEM) ----------------
+ * Replaces: Tile oracle_gemm(const Tile &a, const Tile &b)
+ *           proj/core/include/mimw/oracles.hpp:15-16 (oracles.cpp:14-26).
+ * Host f32 buffers a[m*k], b[k*n] (row-major, B as [K,N]); c[m*n] written. */
+int mimw_b200_oracle_gemm(const float *a, const float *b, float *c, int64_t m, int64_t n,
+                          int64_t k, int32_t precision);
+
+/* Device form: a bf16 [m, lda], b bf16 ([k, ldb] for MIMW_B_KN or [n, ldb]
+ * for MIMW_B_NK), c [m, ldc] of c_dtype (MIMW_F32 or MIMW_BF16).  Leading
+ * dimensions in elements; row pitches must be multiples of 16 bytes (TMA).
+ * Persistent warp-specialized kernel, 2-CTA clusters (cta_group::2). */
+int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_t n, int64_t k,
+                        int64_t lda, int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype,
+                        void *stream);
+
+/* ---- K-gathered GEMM: C = [a0 | a1] . [b0 ; b1] ---------------------------
+ * Replaces: Tile oracle_multi_device_gemm(a0, a1, b0, b1)
+ *           oracles.hpp:24-25 (oracles.cpp:57-80).  Host f32 buffers. */
+int mimw_b200_oracle_multi_device_gemm(const float *a0, const float *a1, const float *b0,
+                                       const float *b1, float *c, int64_t m, int64_t k0,
+                                       int64_t k1, int64_t n, int32_t precision);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIMW_B200_H */

@@ -1,0 +1,174 @@
+"""B200-native (sm_100a) hot path of arXiv 2605.10905 (TLX / MIMW).
+
+Host-side mirror of the reference's operator API
+(/root/reference/proj/core/include/mimw/oracles.hpp) over the C-ABI library
+``libmimw_b200.so`` (include/mimw_b200.h):
+
+* ``oracle_gemm(a, b)``, ``oracle_multi_device_gemm(a0, a1, b0, b1)``,
+  ``oracle_attention(q, k, v, w, scale)``, ``run_oracle(name, inputs,
+  scalars)`` take/return float32 numpy arrays exactly like the reference
+  functions take/return ``Tile`` — same names, same argument meaning.
+  ``run_oracle`` returns ``None`` for an unknown name and raises ``KeyError``
+  for a missing input, as the reference does (oracles.cpp:147-201).
+* ``gemm(...)``, ``attention_fwd(...)`` etc. take CUDA torch tensors (device
+  pointers; torch is plumbing only) and launch on the current stream.
+
+There is NO CPU fallback: importing works anywhere, but every compute call
+raises ``MimwError`` if the library is missing or no B200 is visible.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libmimw_b200.so")
+
+OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4
+F32, BF16 = 0, 1
+B_KN, B_NK = 0, 1
+PREC_BF16, PREC_F32_BF16X3 = 0, 1
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+_fp = C.POINTER(C.c_float)
+
+
+class MimwError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[mimw status {code}] {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libmimw_b200.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MimwError(ERR_CUDA, f"{LIB_PATH} missing: run `python -m paper_2605_10905_b200.build`"
+                                      " (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.mimw_b200_last_error.restype = C.c_char_p
+        L.mimw_b200_version.restype = C.c_int
+        L.mimw_b200_oracle_gemm.argtypes = [_fp, _fp, _fp, _i64, _i64, _i64, C.c_int32]
+        L.mimw_b200_oracle_multi_device_gemm.argtypes = [_fp] * 5 + [_i64] * 4 + [C.c_int32]
+        L.mimw_b200_gemm_bf16.argtypes = [_vp, _vp, _vp] + [_i64] * 6 + [C.c_int32, C.c_int32, _vp]
+        L.mimw_b200_gemm_bf16_ex.argtypes = ([_vp, _vp, _vp] + [_i64] * 6 +
+                                             [C.c_int32] * 5 + [_vp])
+        for name, types in _optional_sigs().items():
+            if hasattr(L, name):
+                getattr(L, name).argtypes = types
+        _lib = L
+    return _lib
+
+
+def _optional_sigs():
+    return {
+        "mimw_b200_oracle_attention": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double],
+        "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
+        "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
+        "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
+    }
+
+
+def _check(status: int) -> None:
+    if status != OK:
+        raise MimwError(status, lib().mimw_b200_last_error().decode(errors="replace"))
+
+
+def _f32(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def _ptr(x: np.ndarray):
+    return x.ctypes.data_as(_fp)
+
+
+# ---------------------------------------------------------------------------
+# reference-signature mirror (host f32 "Tiles")
+# ---------------------------------------------------------------------------
+def oracle_gemm(a, b, precision: int = PREC_BF16) -> np.ndarray:
+    """``Tile oracle_gemm(const Tile &a, const Tile &b)`` (oracles.hpp:15-16)
+    on B200 tensor cores.  ``precision=PREC_F32_BF16X3`` meets the reference's
+    own f32 tolerance (1e-4); the default rounds inputs to bf16 (north-star
+    tolerance 1e-2)."""
+    a, b = _f32(a), _f32(b)
+    m, k = a.shape
+    k2, n = b.shape
+    if k2 != k:
+        raise MimwError(ERR_SHAPE, f"dot conformance: a.shape[1]={k} != b.shape[0]={k2}")
+    c = np.empty((m, n), np.float32)
+    _check(lib().mimw_b200_oracle_gemm(_ptr(a), _ptr(b), _ptr(c), m, n, k, precision))
+    return c
+
+
+def oracle_multi_device_gemm(a0, a1, b0, b1, precision: int = PREC_BF16) -> np.ndarray:
+    """``oracle_multi_device_gemm`` (oracles.hpp:24-25): [a0 | a1] . [b0 ; b1]."""
+    a0, a1, b0, b1 = map(_f32, (a0, a1, b0, b1))
+    m, k0 = a0.shape
+    k1, n = a1.shape[1], b0.shape[1]
+    if a1.shape[0] != m or b0.shape[0] != k0 or b1.shape != (k1, n):
+        raise MimwError(ERR_SHAPE, "multi_device_gemm: inconsistent shapes")
+    c = np.empty((m, n), np.float32)
+    _check(lib().mimw_b200_oracle_multi_device_gemm(_ptr(a0), _ptr(a1), _ptr(b0), _ptr(b1),
+                                                     _ptr(c), m, k0, k1, n, precision))
+    return c
+
+
+def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
+    """``void oracle_attention(q, k, v, int w, double scale, Tile *o)``
+    (oracles.hpp:35-37): windowed causal softmax attention of one [S, D] head."""
+    L = lib()
+    if not hasattr(L, "mimw_b200_oracle_attention"):
+        raise MimwError(ERR_UNSUPPORTED, "attention not built")
+    q, k, v = map(_f32, (q, k, v))
+    s, d = q.shape
+    o = np.empty((s, d), np.float32)
+    lse = np.empty(s, np.float32)
+    _check(L.mimw_b200_oracle_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s, d, w,
+                                        scale))
+    return (o, lse) if with_lse else o
+
+
+def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: int = PREC_BF16):
+    """``run_oracle`` (oracles.cpp:147-201) dispatching to the B200 path for
+    the hot-path oracles.  Unknown / off-path names return ``None``."""
+    scalars = scalars or {}
+    if name == "gemm":
+        return {"c": oracle_gemm(inputs["a"], inputs["b"], precision)}
+    if name == "multi_device_gemm":
+        return {"c": oracle_multi_device_gemm(inputs["a0"], inputs["a1"], inputs["b0"],
+                                              inputs["b1"], precision)}
+    if name == "attention":
+        return {"o": oracle_attention(inputs["q"], inputs["k"], inputs["v"],
+                                      int(scalars.get("w", 1 << 30)), scalars.get("scale", 1.0))}
+    return None
+
+
+# ---------------------------------------------------------------------------
+# device path (torch CUDA tensors as plumbing)
+# ---------------------------------------------------------------------------
+def _stream(stream):
+    import torch
+    return _vp(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+
+
+def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_group: int = 2,
+         raster_group: int = 0, max_clusters: int = 0):
+    """C = A.B with bf16 A [M,K], B [K,N] (B_KN) or [N,K] (B_NK); fp32 accumulate.
+    ``out`` dtype float32 or bfloat16."""
+    import torch
+    m, k = a.shape
+    n = b.shape[1] if b_layout == B_KN else b.shape[0]
+    if out is None:
+        out = torch.empty((m, n), device=a.device, dtype=out_dtype or torch.bfloat16)
+    cd = F32 if out.dtype == torch.float32 else BF16
+    _check(lib().mimw_b200_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k,
+                                        a.stride(0), b.stride(0), out.stride(0), b_layout, cd,
+                                        cta_group, raster_group, max_clusters, _stream(stream)))
+    return out

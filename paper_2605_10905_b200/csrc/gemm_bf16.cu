@@ -1,0 +1,345 @@
+// Persistent warp-specialized bf16 GEMM for sm_100a:  C[M,N] = A[M,K] . B
+//
+// The B200 form of the reference's warp-specialized GEMM programs
+//   proj/kernels/gemm_pipeline.mimw:1-62  (producer task -> smem ring guarded
+//       by ready/free barriers -> consumer async_dot -> global_store)
+//   proj/kernels/gemm_clc.mimw:1-34       (persistent `while tile != -1`)
+//   tests/helpers.hpp:130-146             (collective_dot across a CTA pair)
+// computing oracle_gemm (proj/core/src/oracles.cpp:14-26) with fp32
+// accumulation in TMEM.
+//
+// MIMW roles (one CTA = 6 warps, one CTA per SM, CG CTAs per cluster):
+//   warp 0      TMA producer: waits `empty[s]`, arms `full[s]` with the
+//               stage's byte count, issues cp.async.bulk.tensor loads
+//               (barrier_expect / async_copy in the reference).
+//   warp 1      TMEM allocator + MMA issuer (leader CTA only): one elected
+//               thread issues tcgen05.mma (cta_group::CG), tcgen05.commit
+//               frees the smem slot and, per tile, fills `tmem_full[acc]`.
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bf16/f32 ->
+//               swizzled smem -> TMA store; arrive `tmem_empty[acc]` on the
+//               leader so the next tile's MMAs can reuse the accumulator.
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap
+// the main loop of tile i+1.
+//
+// CG = 2: a CTA pair runs M=256 tcgen05.mma.cta_group::2.  Each CTA stages
+// its own 128 rows of A and half of B's N columns; the hardware combines
+// them (the reference's collective_dot replicates B instead,
+// sim.cpp:1322-1338 — same product, half the smem traffic).  All TMA loads
+// of the pair complete on the leader's `full[s]`; the leader's commits are
+// multicast to both CTAs' `empty[s]` / `tmem_full[acc]`.
+#include "gemm_bf16.h"
+#include "ptx.cuh"
+#include "tma_host.h"
+
+namespace mimw {
+
+namespace {
+
+constexpr int BK = 64;           // K per stage (one 128-byte swizzle row of bf16)
+constexpr int UMMA_K = 16;       // K per tcgen05.mma (kind::f16)
+constexpr int BN = 256;          // N per MMA / per cluster tile
+constexpr int BM_CTA = 128;      // rows of A per CTA
+constexpr int EPI_WARPS = 4;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int ACC_STAGES = 2;    // TMEM accumulators (2 x 256 columns = 512)
+constexpr int EPI_COLS = 32;     // columns per epilogue store chunk
+
+template <int CG, bool B_MN, typename OutT>
+struct Cfg {
+  static constexpr int NB_CTA = BN / CG;                       // B columns staged per CTA
+  static constexpr int A_BYTES = BM_CTA * BK * 2;              // 16 KiB
+  static constexpr int B_BYTES = NB_CTA * BK * 2;              // 16 / 32 KiB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (CG == 2) ? 6 : 4;
+  static constexpr int EPI_BUF = 32 * EPI_COLS * (int)sizeof(OutT);   // per warp per buffer
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES + EPI_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;            // + barriers + align slack
+  static constexpr uint32_t IDESC = idesc_bf16(BM_CTA * CG, BN, 0, B_MN ? 1 : 0);
+};
+
+struct Sched {
+  int num_m, num_n, group;
+  __device__ __forceinline__ void tile(int t, int &mt, int &nt) const {
+    int per_group = group * num_n;
+    int g = t / per_group;
+    int first_m = g * group;
+    int gsize = min(num_m - first_m, group);
+    int r = t - g * per_group;
+    mt = first_m + r % gsize;
+    nt = r / gsize;
+  }
+};
+
+template <int CG, bool B_MN, typename OutT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, int M, int N, int K, Sched sched) {
+  using C = Cfg<CG, B_MN, OutT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_base = sbase + C::BAR_OFF;
+  auto full_bar = [&](int s) { return bar_base + 8 * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8 * (C::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + ACC_STAGES + a); };
+  const uint32_t tmem_slot = bar_base + 8 * (2 * C::STAGES + 2 * ACC_STAGES);
+  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * C::STAGES + 2 * ACC_STAGES));
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = (rank == 0);
+  const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
+  const int num_tiles = sched.num_m * sched.num_n;
+  const int num_k = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < ACC_STAGES; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), EPI_WARPS * CG);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<CG>(tmem_slot, 512);
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), 0) : full_bar(0);
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        int mt, nt;
+        sched.tile(t, mt, nt);
+        const int m0 = mt * BM_CTA * CG + (int)rank * BM_CTA;
+        const int n0 = nt * BN + (int)rank * C::NB_CTA;
+        for (int kb = 0; kb < num_k; ++kb) {
+          if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
+          else mbar_wait(empty_bar(stage), phase ^ 1, 1);
+          const uint32_t fb = full_target0 + 8 * stage;
+          if (leader) mbar_arrive_expect_tx(full_bar(stage), C::STAGE_BYTES * CG);
+          const uint32_t sa = sbase + stage * C::STAGE_BYTES;
+          const uint32_t sb = sa + C::A_BYTES;
+          const int k0 = kb * BK;
+          if constexpr (CG == 2) {
+            tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < C::NB_CTA / 64; ++j)
+                tma_load_2d_cg2(sb + j * (64 * BK * 2), &tmB, fb, n0 + j * 64, k0);
+            } else {
+              tma_load_2d_cg2(sb, &tmB, fb, k0, n0);
+            }
+          } else {
+            tma_load_2d(sa, &tmA, fb, k0, m0);
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < C::NB_CTA / 64; ++j)
+                tma_load_2d(sb + j * (64 * BK * 2), &tmB, fb, n0 + j * 64, k0);
+            } else {
+              tma_load_2d(sb, &tmB, fb, k0, n0);
+            }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1, 2);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(full_bar(stage), phase, 3);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = sbase + stage * C::STAGE_BYTES;
+            const uint32_t sb = sa + C::A_BYTES;
+            const uint64_t adesc = smem_desc_sw128(sa, 16, 1024);
+            const uint64_t bdesc = B_MN ? smem_desc_sw128(sb, 64 * BK * 2, 1024)
+                                        : smem_desc_sw128(sb, 16, 1024);
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              // K-major A: +32 B per K=16 inside the 128-B swizzle row.
+              // MN-major B: +16 rows x 128 B per K=16.  K-major B: +32 B.
+              const uint64_t a_k = adesc + (uint64_t)((k * UMMA_K * 2) >> 4);
+              const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((k * UMMA_K * 128) >> 4)
+                                                          : ((k * UMMA_K * 2) >> 4));
+              mma_f16_ss<CG>(d_tmem, a_k, b_k, C::IDESC, (kb | k) != 0);
+            }
+            if constexpr (CG == 2) {
+              mma_commit_cg2_mc(empty_bar(stage), 0x3);
+              if (kb == num_k - 1) mma_commit_cg2_mc(tfull_bar(acc), 0x3);
+            } else {
+              mma_commit(empty_bar(stage));
+              if (kb == num_k - 1) mma_commit(tfull_bar(acc));
+            }
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps ----------------
+    const int q = warp & 3;                         // TMEM lane quarter this warp may access
+    const int ew = warp - 2;                        // epilogue warp index (staging buffers)
+    const uint32_t lane = lane_id();
+    const uint32_t stage_base = sbase + C::STAGES * C::STAGE_BYTES + ew * 2 * C::EPI_BUF;
+    const uint32_t tempty_leader0 = (CG == 2) ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int buf = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      int mt, nt;
+      sched.tile(t, mt, nt);
+      const int row0 = mt * BM_CTA * CG + (int)rank * BM_CTA + q * 32;
+      const int col0 = nt * BN;
+      mbar_wait(tfull_bar(acc), acc_phase, 4);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / EPI_COLS; ++ch) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + ch * EPI_COLS, v);
+        tmem_ld_wait();
+        if (ch == BN / EPI_COLS - 1) {
+          // accumulator fully drained into registers: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + 8 * acc);
+            else mbar_arrive(tempty_bar(acc));
+          }
+        }
+        const bool live = (row0 < M) && (col0 + ch * EPI_COLS < N);
+        if (live) {
+          // staging buffer `buf` was used two chunks ago: its store must have read smem
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          const uint32_t sbuf = stage_base + buf * C::EPI_BUF;
+          if constexpr (sizeof(OutT) == 2) {
+            // 32 rows x 64 B, SWIZZLE_64B: 16-B chunk c of row r at c ^ ((r >> 1) & 3)
+            const uint32_t rbase = sbuf + lane * 64;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t pc = (uint32_t)c ^ ((lane >> 1) & 3);
+              st_shared_v4(rbase + pc * 16,
+                           pack_bf16(__uint_as_float(v[8 * c + 0]), __uint_as_float(v[8 * c + 1])),
+                           pack_bf16(__uint_as_float(v[8 * c + 2]), __uint_as_float(v[8 * c + 3])),
+                           pack_bf16(__uint_as_float(v[8 * c + 4]), __uint_as_float(v[8 * c + 5])),
+                           pack_bf16(__uint_as_float(v[8 * c + 6]), __uint_as_float(v[8 * c + 7])));
+            }
+          } else {
+            // 32 rows x 128 B, SWIZZLE_128B: 16-B chunk c of row r at c ^ (r & 7)
+            const uint32_t rbase = sbuf + lane * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t pc = (uint32_t)c ^ (lane & 7);
+              st_shared_v4(rbase + pc * 16, v[4 * c + 0], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, sbuf, col0 + ch * EPI_COLS, row0);
+            bulk_commit();
+          }
+          buf ^= 1;
+        }
+      }
+      if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<CG>(tmem_base, 512);
+  }
+}
+
+template <int CG, bool B_MN, typename OutT>
+cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
+  using C = Cfg<CG, B_MN, OutT>;
+  const CUtensorMapDataType cdt =
+      sizeof(OutT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.k, g.lda, BK,
+                                BM_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tB = B_MN ? make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, g.ldb,
+                                       64, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                        : make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, g.ldb,
+                                       BK, C::NB_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tC = make_tmap_2d(g.c, cdt, sizeof(OutT), g.m, g.n, g.ldc, EPI_COLS, 32,
+                                sizeof(OutT) == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_128B);
+  Sched s;
+  s.num_m = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
+  s.num_n = (int)((g.n + BN - 1) / BN);
+  s.group = g.raster_group > 0 ? g.raster_group : 8;
+  const int tiles = s.num_m * s.num_n;
+  int clusters = sm_count() / CG;
+  if (g.max_clusters > 0 && g.max_clusters < clusters) clusters = g.max_clusters;
+  if (clusters > tiles) clusters = tiles;
+
+  auto kern = gemm_bf16_kernel<CG, B_MN, OutT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, (int)g.m, (int)g.n, (int)g.k, s);
+}
+
+}  // namespace
+
+cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream) {
+  if (g.k == 0) {
+    // no K: C = 0 (the oracle's float accumulator starts at 0.0f, oracles.cpp:19)
+    size_t es = g.c_f32 ? 4 : 2;
+    return cudaMemset2DAsync(g.c, g.ldc * es, 0, g.n * es, g.m, stream);
+  }
+  const bool cg2 = g.cta_group != 1;
+  if (g.b_kn) {
+    if (g.c_f32) return cg2 ? launch_impl<2, true, float>(g, stream) : launch_impl<1, true, float>(g, stream);
+    return cg2 ? launch_impl<2, true, __nv_bfloat16>(g, stream)
+               : launch_impl<1, true, __nv_bfloat16>(g, stream);
+  }
+  if (g.c_f32) return cg2 ? launch_impl<2, false, float>(g, stream) : launch_impl<1, false, float>(g, stream);
+  return cg2 ? launch_impl<2, false, __nv_bfloat16>(g, stream)
+             : launch_impl<1, false, __nv_bfloat16>(g, stream);
+}
+
+}  // namespace mimw

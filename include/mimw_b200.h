@@ -73,6 +73,25 @@ int mimw_b200_oracle_multi_device_gemm(const float *a0, const float *a1, const f
                                        const float *b1, float *c, int64_t m, int64_t k0,
                                        int64_t k1, int64_t n, int32_t precision);
 
+/* ---- Attention forward (windowed causal softmax attention) --------------
+ * Replaces: void oracle_attention(const Tile &q, const Tile &k, const Tile &v,
+ *                                 int w, double scale, Tile *o)
+ *           oracles.hpp:35-37 (oracles.cpp:119-145): keys j in
+ *           [max(0, i-w+1), i]; w >= seq is plain causal attention.
+ * Host f32 buffers q, k, v, o of [seq, d] (d <= 128; zero-padded to 128
+ * internally, exact); lse[seq] (natural-log logsumexp of the scaled scores,
+ * as oracle_simplicial_attention's lse, oracles.cpp:116) may be NULL. */
+int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, float *o,
+                               float *lse, int64_t seq, int64_t d, int64_t w, double scale);
+
+/* Device form: q, k, v, o bf16 [batch, heads, seq, head_dim] contiguous,
+ * head_dim == 128; lse fp32 [batch, heads, seq] or NULL.  Warp-specialized
+ * kernel: TMA producer warp, single-thread tcgen05 MMA warp (S = QK^T and
+ * O += PV with P in TMEM), two ping-pong softmax/correction warpgroups. */
+int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o, float *lse,
+                            int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
+                            int64_t window, double scale, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,8 @@ def _declare_c(lib):
     lib.orc_multi_device_gemm.argtypes = [_f32p] * 5 + [_i64] * 4
     lib.orc_attention.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p,
                                   _i64, _i64, _i64, C_.c_double]
+    lib.orc_attention_rows.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p,
+                                       _i64, _i64, _i64, C_.c_double, _i64, _i64]
     lib.orc_simplicial_attention.argtypes = [_f32p] * 7 + [_i64] * 4 + [C_.c_double]
     lib.orc_layernorm.argtypes = [_f32p, _f32p, _f32p, C_.c_double, _f32p,
                                   _f32p, _f32p, _i64, _i64]
@@ -181,6 +183,17 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
     lse = np.empty(s, np.float32) if with_lse else None
     C.orc_attention(q, k, v, o, lse.ctypes.data if with_lse else None, s, d, w, scale)
     return (o, lse) if with_lse else o
+
+
+def oracle_attention_rows(q, k, v, w: int, scale: float, r0: int, r1: int):
+    """Rows [r0, r1) of oracle_attention (exact: rows are independent in
+    oracles.cpp:123-144).  Returns (o[r1-r0, D], lse[r1-r0])."""
+    q, k, v = map(_f32, (q, k, v))
+    s, d = q.shape
+    o = np.empty((r1 - r0, d), np.float32)
+    lse = np.empty(r1 - r0, np.float32)
+    C.orc_attention_rows(q, k, v, o, lse.ctypes.data, s, d, w, scale, r0, r1)
+    return o, lse
 
 
 def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float):

@@ -203,11 +203,16 @@ void orc_multi_device_gemm(const float *a0, const float *a1, const float *b0,
  * in ascending j with a float accumulator.  lse (not produced by the
  * reference function) is m + log(l) as in oracles.cpp:116, written only when
  * lse != NULL. */
-void orc_attention(const float *q, const float *k, const float *v, float *o,
-                   float *lse, int64_t seq, int64_t d, int64_t w, double scale) {
+/* Rows [r0, r1) only (each row of the reference loop is independent); o and
+ * lse are indexed from row r0.  Used for row-sampled parity at S = 8192. */
+void orc_attention_rows(const float *q, const float *k, const float *v, float *o,
+                        float *lse, int64_t seq, int64_t d, int64_t w, double scale,
+                        int64_t r0, int64_t r1) {
   double *scores = (double *)malloc(sizeof(double) * (size_t)(seq > 0 ? seq : 1));
-  memset(o, 0, sizeof(float) * (size_t)(seq * d));
-  for (int64_t i = 0; i < seq; ++i) {
+  memset(o, 0, sizeof(float) * (size_t)((r1 - r0) * d));
+  o -= r0 * d;
+  if (lse) lse -= r0;
+  for (int64_t i = r0; i < r1; ++i) {
     int64_t j0 = i - w + 1 > 0 ? i - w + 1 : 0;
     int64_t cnt = 0;
     for (int64_t j = j0; j <= i; ++j) {
@@ -227,6 +232,11 @@ void orc_attention(const float *q, const float *k, const float *v, float *o,
     if (lse) lse[i] = (float)(m + log(l));
   }
   free(scores);
+}
+
+void orc_attention(const float *q, const float *k, const float *v, float *o,
+                   float *lse, int64_t seq, int64_t d, int64_t w, double scale) {
+  orc_attention_rows(q, k, v, o, lse, seq, d, w, scale, 0, seq);
 }
 
 /* Trilinear attention with asymmetric causal windows

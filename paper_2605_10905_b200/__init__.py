@@ -172,3 +172,26 @@ def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_
                                         a.stride(0), b.stride(0), out.stride(0), b_layout, cd,
                                         cta_group, raster_group, max_clusters, _stream(stream)))
     return out
+
+
+def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None, out=None,
+                  lse=None, want_lse: bool = True, stream=None):
+    """Causal (optionally windowed) attention forward on bf16 [B, H, S, 128]
+    CUDA tensors.  Returns (o, lse) with lse fp32 [B, H, S] (natural log)."""
+    import torch
+    b, h, s, d = q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None and want_lse:
+        lse = torch.empty((b, h, s), device=q.device, dtype=torch.float32)
+    if scale is None:
+        scale = d ** -0.5
+    if window is None:
+        window = s
+    for t in (q, k, v, out):
+        if not t.is_contiguous():
+            raise MimwError(ERR_UNSUPPORTED, "attention_fwd needs contiguous [B,H,S,D] tensors")
+    _check(lib().mimw_b200_attention_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                         lse.data_ptr() if lse is not None else None, b, h, s, d,
+                                         window, scale, _stream(stream)))
+    return out, lse

@@ -1,0 +1,20 @@
+// Internal launcher interface for the warp-specialized flash-attention forward.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mimw {
+
+struct AttnArgs {
+  const void *q, *k, *v;  // [batch, heads, seq, 128] bf16, contiguous
+  void *o;                // [batch, heads, seq, 128] bf16
+  float *lse;             // [batch, heads, seq] fp32 (natural log) or null
+  int64_t batch, heads, seq;
+  int64_t window;         // keys j in [i - window + 1, i]; >= seq means plain causal
+  double scale;
+  int max_ctas;           // 0 = one persistent CTA per SM
+};
+
+cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream);
+
+}  // namespace mimw

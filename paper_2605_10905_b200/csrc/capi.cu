@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -14,6 +16,7 @@
 
 #include "../../include/mimw_b200.h"
 #include "convert.h"
+#include "attention_fwd.h"
 #include "gemm_bf16.h"
 
 namespace {
@@ -166,6 +169,55 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   check_cuda(cudaStreamSynchronize(s), "gemm execution");
 }
 
+
+// o[s,d] (+ lse[s]) = oracle_attention(q, k, v, w, scale) for one head of
+// host f32 Tiles (oracles.cpp:119-145).  Head dim is zero-padded to 128 (exact:
+// padded q/k columns add 0 to every score, padded v columns give 0 outputs).
+void host_attention(const float *q, const float *k, const float *v, float *o, float *lse,
+                    int64_t seq, int64_t d, int64_t w, double scale) {
+  require(seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
+  require(w >= 1 || seq == 0, MIMW_ERR_ARG, "window must be >= 1");
+  if (seq == 0 || d == 0) {
+    if (o && seq) std::memset(o, 0, sizeof(float) * seq * d);
+    if (lse && seq && d == 0)
+      for (int64_t i = 0; i < seq; ++i) lse[i] = std::log((float)std::min<int64_t>(w, i + 1));
+    return;
+  }
+  require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
+  require_sm100();
+  cudaStream_t s = cudaStreamPerThread;
+  const int64_t n = seq * d;
+  DevBuf din(sizeof(float) * 3 * n, s);
+  DevBuf dq(2 * seq * 128, s), dk(2 * seq * 128, s), dv(2 * seq * 128, s), dout(2 * seq * 128, s);
+  DevBuf dlse(sizeof(float) * seq, s), dof(sizeof(float) * n, s);
+  float *f = din.as<float>();
+  check_cuda(cudaMemcpyAsync(f, q, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D q");
+  check_cuda(cudaMemcpyAsync(f + n, k, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D k");
+  check_cuda(cudaMemcpyAsync(f + 2 * n, v, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D v");
+  mimw::stage_cols_bf16(f, seq, d, 128, dq.p, 128, 0, 0, s);
+  mimw::stage_cols_bf16(f + n, seq, d, 128, dk.p, 128, 0, 0, s);
+  mimw::stage_cols_bf16(f + 2 * n, seq, d, 128, dv.p, 128, 0, 0, s);
+  check_cuda(cudaGetLastError(), "staging kernels");
+  mimw::AttnArgs a{};
+  a.q = dq.p;
+  a.k = dk.p;
+  a.v = dv.p;
+  a.o = dout.p;
+  a.lse = dlse.as<float>();
+  a.batch = 1;
+  a.heads = 1;
+  a.seq = seq;
+  a.window = w;
+  a.scale = scale;
+  check_cuda(mimw::attention_fwd_launch(a, s), "attention launch");
+  mimw::unpad_bf16_to_f32(dout.p, 128, dof.as<float>(), seq, d, s);
+  check_cuda(cudaGetLastError(), "unpad");
+  check_cuda(cudaMemcpyAsync(o, dof.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H o");
+  if (lse) check_cuda(cudaMemcpyAsync(lse, dlse.p, sizeof(float) * seq, cudaMemcpyDeviceToHost, s), "D2H lse");
+  check_cuda(cudaStreamSynchronize(s), "attention execution");
+}
+
 }  // namespace
 
 extern "C" {
@@ -222,6 +274,39 @@ int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_
     g.c_f32 = c_dtype == MIMW_F32;
     g.cta_group = 2;
     check_cuda(mimw::gemm_bf16_launch(g, static_cast<cudaStream_t>(stream)), "gemm launch");
+  });
+}
+
+int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, float *o, float *lse,
+                               int64_t seq, int64_t d, int64_t w, double scale) {
+  return guarded([&] { host_attention(q, k, v, o, lse, seq, d, w, scale); });
+}
+
+int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o, float *lse,
+                            int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
+                            int64_t window, double scale, void *stream) {
+  return guarded([&] {
+    require(batch >= 0 && heads >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
+    require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device attention supports head_dim == 128");
+    require(window >= 1, MIMW_ERR_ARG, "window must be >= 1");
+    require(seq < (1ll << 31) && batch * heads < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
+    if (batch == 0 || heads == 0 || seq == 0) return;
+    require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
+    require(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) % 16 == 0, MIMW_ERR_UNSUPPORTED,
+            "tensors must be 16-byte aligned");
+    require_sm100();
+    mimw::AttnArgs a{};
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.o = o;
+    a.lse = lse;
+    a.batch = batch;
+    a.heads = heads;
+    a.seq = seq;
+    a.window = window;
+    a.scale = scale;
+    check_cuda(mimw::attention_fwd_launch(a, static_cast<cudaStream_t>(stream)), "attention launch");
   });
 }
 

@@ -59,6 +59,16 @@ __global__ void unpad_f32_kernel(const float *__restrict__ src, int64_t ld, floa
   }
 }
 
+__global__ void unpad_bf16_kernel(const __nv_bfloat16 *__restrict__ src, int64_t ld,
+                                  float *__restrict__ dst, int64_t rows, int64_t cols) {
+  int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / cols, c = i - r * cols;
+    dst[i] = __bfloat162float(src[r * ld + c]);
+  }
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)(g < 4096 ? (g > 0 ? g : 1) : 4096);
@@ -82,6 +92,12 @@ void stage_rows_bf16(const float *src, int64_t rows, int64_t pad_rows, int64_t c
 void unpad_f32(const float *src, int64_t ld, float *dst, int64_t rows, int64_t cols,
                cudaStream_t s) {
   unpad_f32_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, ld, dst, rows, cols);
+}
+
+void unpad_bf16_to_f32(const void *src, int64_t ld, float *dst, int64_t rows, int64_t cols,
+                       cudaStream_t s) {
+  unpad_bf16_kernel<<<grid_for(rows * cols), 256, 0, s>>>(static_cast<const __nv_bfloat16 *>(src), ld,
+                                                           dst, rows, cols);
 }
 
 }  // namespace mimw

@@ -11,4 +11,6 @@ void stage_rows_bf16(const float *src, int64_t rows, int64_t pad_rows, int64_t c
                      cudaStream_t s);
 void unpad_f32(const float *src, int64_t ld, float *dst, int64_t rows, int64_t cols,
                cudaStream_t s);
+void unpad_bf16_to_f32(const void *src, int64_t ld, float *dst, int64_t rows, int64_t cols,
+                       cudaStream_t s);
 }  // namespace mimw

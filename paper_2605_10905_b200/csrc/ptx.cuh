@@ -120,7 +120,7 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
   return ok != 0;
 }
 
-__device__ __noinline__ void watchdog_trap(uint32_t bar, uint32_t parity, int tag) {
+static __device__ __noinline__ void watchdog_trap(uint32_t bar, uint32_t parity, int tag) {
   printf("mimw watchdog: block (%d,%d) thread %d stuck on mbarrier 0x%x parity %u tag %d\n",
          blockIdx.x, blockIdx.y, threadIdx.x, bar, parity, tag);
   asm volatile("trap;");

@@ -27,7 +27,7 @@ def L():
 def test_header_declares_the_reference_replacements():
     names = _declared()
     for n in ("mimw_b200_oracle_gemm", "mimw_b200_oracle_multi_device_gemm",
-              "mimw_b200_gemm_bf16",
+              "mimw_b200_oracle_attention", "mimw_b200_gemm_bf16", "mimw_b200_attention_fwd",
               "mimw_b200_last_error", "mimw_b200_version"):
         assert n in names, n
 

@@ -154,3 +154,10 @@ def test_attention_live_vs_reference(s, d, w):
     want = np.empty((s, d), np.float32)
     oracle.REF.ref_oracle_attention(q, k, v, want, s, d, w, 0.3)
     assert oracle.rel_error(oracle.oracle_attention(q, k, v, w, 0.3), want) <= 1e-6
+
+
+def test_attention_rows_matches_full():
+    q, k, v = (oracle.random_tile([70, 24], 200 + i) for i in range(3))
+    o, lse = oracle.oracle_attention(q, k, v, 30, 0.2, with_lse=True)
+    orow, lrow = oracle.oracle_attention_rows(q, k, v, 30, 0.2, 33, 61)
+    assert np.array_equal(orow, o[33:61]) and np.array_equal(lrow, lse[33:61])

@@ -302,15 +302,69 @@ def bench_gemm(args, rank, ws, local):
     return res
 
 
+def bench_attention(args, rank, ws, local):
+    """configs[3]: causal FA forward bf16 B=4 H=32 S=8192 D=128, batch x head
+    sharded over the ranks (strong scaling: each rank runs B*H/N heads)."""
+    import torch
+    import paper_2605_10905_b200 as P
+    L = P.lib()
+    pk = peaks()
+    dev = torch.device("cuda", local)
+    bh = FA_B * FA_H
+    assert bh % ws == 0
+    my = bh // ws
+    g = torch.Generator(device=dev).manual_seed(31 + rank)
+    q, k, v = ((torch.rand((my, 1, FA_S, FA_D), device=dev, generator=g) * 2 - 1)
+               .to(torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    lse = torch.empty((my, 1, FA_S), device=dev, dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    scale = FA_D ** -0.5
+
+    def step():
+        P._check(L.mimw_b200_attention_fwd_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                              lse.data_ptr(), my, 1, FA_S, FA_S, scale, args.fa_emu,
+                                              0, None, sptr))
+
+    steps = max(3, args.steps // 5)
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(step, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    flop_total = 4.0 * bh * FA_D * FA_S * FA_S / 2  # FA causal convention (SURVEY §8d)
+    flop_mine = flop_total / ws
+    value = flop_total * steps / secs / 1e12
+    achieved = flop_mine / (secs / steps) / 1e12
+    res = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": round(secs / steps * 1e3, 4),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic U[-1,1] bf16",
+           "config": {"workload": "configs[3]: causal flash-attention forward bf16 B=4 H=32 "
+                                  "S=8192 D=128, batch x head sharded",
+                      "B": FA_B, "H": FA_H, "S": FA_S, "D": FA_D,
+                      "parallelism": f"{my} of {bh} heads per GPU",
+                      "l2": "Q,K,V 3 x 256 MiB > 126 MB L2 (no flush)"},
+           "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
+                        "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
+                        "frac_of_spec_2250": round(achieved / 2250.0, 4),
+                        "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
+                        "traffic": None, "algorithmic_flop_per_launch": flop_mine},
+           "gpu_launches": steps, "clocks": clocks}
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm"])
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--fa-emu", type=int, default=-1, help="exp2 pairs of 8 on the FMA pipe")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -342,7 +396,14 @@ def main():
         return
 
     rank, ws, local = dist_init(args.gpus)
-    res = bench_gemm(args, rank, ws, local)
+    if args.workload == "attention":
+        res = bench_attention(args, rank, ws, local)
+    else:
+        res = bench_gemm(args, rank, ws, local)
+        if not args.no_secondary:
+            fa = bench_attention(args, rank, ws, local)
+            res["secondary"] = {"attention_fwd": {k: fa[k] for k in (
+                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks")}}
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

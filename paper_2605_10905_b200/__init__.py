@@ -71,6 +71,8 @@ def _optional_sigs():
     return {
         "mimw_b200_oracle_attention": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double],
         "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
+        "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
+                                                                           C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
     }
@@ -175,7 +177,8 @@ def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_
 
 
 def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None, out=None,
-                  lse=None, want_lse: bool = True, stream=None):
+                  lse=None, want_lse: bool = True, stream=None, emu: int = -1, max_ctas: int = 0,
+                  trace=None):
     """Causal (optionally windowed) attention forward on bf16 [B, H, S, 128]
     CUDA tensors.  Returns (o, lse) with lse fp32 [B, H, S] (natural log)."""
     import torch
@@ -191,7 +194,11 @@ def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None
     for t in (q, k, v, out):
         if not t.is_contiguous():
             raise MimwError(ERR_UNSUPPORTED, "attention_fwd needs contiguous [B,H,S,D] tensors")
-    _check(lib().mimw_b200_attention_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                                         lse.data_ptr() if lse is not None else None, b, h, s, d,
-                                         window, scale, _stream(stream)))
+    if d != 128:
+        raise MimwError(ERR_UNSUPPORTED, "device attention supports head_dim == 128")
+    _check(lib().mimw_b200_attention_fwd_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                            lse.data_ptr() if lse is not None else None, b, h, s,
+                                            window, scale, emu, max_ctas,
+                                            trace.data_ptr() if trace is not None else None,
+                                            _stream(stream)))
     return out, lse

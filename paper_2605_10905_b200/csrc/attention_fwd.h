@@ -13,6 +13,8 @@ struct AttnArgs {
   int64_t window;         // keys j in [i - window + 1, i]; >= seq means plain causal
   double scale;
   int max_ctas;           // 0 = one persistent CTA per SM
+  unsigned long long *trace = nullptr;  // optional [grid][12 warps][8] cycle counters
+  int emu = -1;           // exp2 pairs of 8 on the FMA pipe (-1 = default)
 };
 
 cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream);

@@ -310,6 +310,35 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
   });
 }
 
+// Tuning hook (not part of the public header): attention with an explicit
+// exp2-emulation split and CTA cap.
+int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void *o, float *lse,
+                               int64_t batch, int64_t heads, int64_t seq, int64_t window,
+                               double scale, int32_t emu, int32_t max_ctas, void *trace,
+                               void *stream) {
+  return guarded([&] {
+    if (batch == 0 || heads == 0 || seq == 0) return;
+    require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
+    require(window >= 1, MIMW_ERR_ARG, "window must be >= 1");
+    require_sm100();
+    mimw::AttnArgs a{};
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.o = o;
+    a.lse = lse;
+    a.batch = batch;
+    a.heads = heads;
+    a.seq = seq;
+    a.window = window;
+    a.scale = scale;
+    a.emu = emu;
+    a.max_ctas = max_ctas;
+    a.trace = static_cast<unsigned long long *>(trace);
+    check_cuda(mimw::attention_fwd_launch(a, static_cast<cudaStream_t>(stream)), "attention launch");
+  });
+}
+
 // Tuning / test hook (not part of the public header): force cta_group and
 // raster group.  Used by the parity tests to cover the 1-CTA variant.
 int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int64_t n, int64_t k,

@@ -120,9 +120,17 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
   return ok != 0;
 }
 
-static __device__ __noinline__ void watchdog_trap(uint32_t bar, uint32_t parity, int tag) {
-  printf("mimw watchdog: block (%d,%d) thread %d stuck on mbarrier 0x%x parity %u tag %d\n",
-         blockIdx.x, blockIdx.y, threadIdx.x, bar, parity, tag);
+// Diagnostic record of the first watchdog hit (read back by the host on a
+// launch failure).  No printf/call here: a call site would force the caller's
+// live registers through the ABI, which breaks setmaxnreg register budgets.
+__device__ uint32_t g_mimw_watchdog[4];
+
+static __device__ __forceinline__ void watchdog_trap(uint32_t bar, uint32_t parity, int tag) {
+  g_mimw_watchdog[0] = 1u;
+  g_mimw_watchdog[1] = bar;
+  g_mimw_watchdog[2] = parity;
+  g_mimw_watchdog[3] = (uint32_t)tag | (blockIdx.x << 8);
+  __threadfence_system();
   asm volatile("trap;");
 }
 

@@ -78,6 +78,7 @@ def test_device_gemm_1024_full_oracle(P, cta_group, b_layout, out):
                out_dtype=torch.float32 if out == "f32" else torch.bfloat16)
     torch.cuda.synchronize()
     got = c.float().cpu().numpy()
+    assert np.isfinite(got).all()
     tol = BF16_TOL
     assert oracle.rel_error(got, want) <= tol
     assert oracle.rel_error_rows(got, want) <= tol

@@ -1,0 +1,56 @@
+// Microbenchmark: tcgen05.mma issue->completion rate for the FA shapes.
+// One CTA per SM, one thread issues `iters` MMAs of a given kind into TMEM and
+// waits on the commit barrier; reports cycles per MMA (K=16).
+#include <cstdio>
+#include "../paper_2605_10905_b200/csrc/ptx.cuh"
+using namespace mimw;
+
+template <int MODE>  // 0: SS M128 N128, 1: TS M128 N128, 2: SS M128 N256, 3: SS M128 N64
+__global__ void __launch_bounds__(128, 1) k(long long *out, int iters) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  uint32_t sb = smem_u32(sm);
+  sb = (sb + 1023) & ~1023u;
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc<1>(smem_u32(&slot), 512);
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    constexpr int N = MODE == 2 ? 256 : (MODE == 3 ? 64 : 128);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint64_t a = smem_desc_sw128(sb + (i & 3) * 32, 16, 1024);
+      const uint64_t b = smem_desc_sw128(sb + 32768 + (i & 3) * 32, 16, 1024);
+      if (MODE == 1) mma_f16_ts<1>(tm + 256, tm + (i & 7) * 8, b, id, 1);
+      else mma_f16_ss<1>(tm, a, b, id, 1);
+    }
+    mma_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<1>(tm, 512); }
+}
+
+int main() {
+  long long *d; cudaMalloc(&d, 148 * 8);
+  long long h[148];
+  const int iters = 4096;
+  auto run = [&](auto kern, const char *name, int n) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+    kern<<<148, 128, 100000>>>(d, iters);
+    kern<<<148, 128, 100000>>>(d, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
+    printf("%-22s %s cycles/MMA %.1f  (ideal %d)\n", name, cudaGetErrorString(e), avg / iters, n);
+  };
+  run(k<0>, "SS M128 N128 K16", 64);
+  run(k<1>, "TS M128 N128 K16", 64);
+  run(k<2>, "SS M128 N256 K16", 128);
+  run(k<3>, "SS M128 N64 K16", 32);
+  return 0;
+}

@@ -24,7 +24,8 @@ LIB = os.path.join(PKG, "libmimw_b200.so")
 ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+DEBUG = ["-DMIMW_WATCHDOG_PRINTF"] if os.environ.get("MIMW_DEBUG") else []
+FLAGS = DEBUG + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                 "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 
 

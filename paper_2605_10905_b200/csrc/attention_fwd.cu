@@ -7,26 +7,28 @@
 // does (oracles.cpp:116, simplicial_attention.mimw:88-93).
 //
 // MIMW structure (the B200 form of proj/kernels/simplicial_attention.mimw:
-// producer task staging K/V blocks through barriers + consumer online
-// softmax), one persistent CTA per SM, 10 warps:
-//   warps 0-3  softmax WG 0 : Q tile 0 (rows q0 .. q0+127), one row per thread
-//   warps 4-7  softmax WG 1 : Q tile 1 (rows q0+128 .. q0+255)  (ping-pong)
-//   warp 8     TMA producer : Q0, Q1, then K_j / V_j through a 5-slot ring
-//   warp 9     MMA issuer   : S_h = Q_h K_j^T (SS-MMA into TMEM),
-//                             O_h += P_h V_j (TS-MMA, P read from TMEM)
-// The softmax WG owning Q tile h also performs the online-softmax correction
-// (conditional O rescale in TMEM when the running max grows by > 2^8) and the
-// epilogue (O / l -> bf16 -> smem -> TMA store, lse -> HBM).
+// a producer task staging K/V blocks through barriers, consumers running an
+// online softmax), one persistent CTA per SM, 12 warps in 3 warpgroups:
+//   WG0 (warps 0-3)  softmax/correction for Q tile 0 (rows q0 .. q0+127)
+//   WG1 (warps 4-7)  softmax/correction for Q tile 1 (rows q0+128 .. q0+255)
+//   WG2 warp 8       TMA producer + tile scheduler (atomic work counter,
+//                    published through a 2-slot mbarrier ring: the CLC
+//                    clc_producer/clc_consumer protocol of sim.cpp:1213-1286)
+//   WG2 warp 9       MMA issuer: S = Q_h K_j^T (SS) and O_h += P_h V_j (TS)
+//   WG2 warps 10-11  idle (donate registers via setmaxnreg)
 //
-// MMA issue order per KV step j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1).
-// tcgen05 ops of one thread complete in order and a commit covers all prior
-// ops, so when softmax h sees S_h(j+1) complete, PV_h(j) is complete too:
-// O_h is stable for the in-place rescale without an extra barrier, and P_h(j)
-// (which aliases S_h's TMEM columns) has been consumed before S_h(j+1)
-// overwrites it.
-//
-// TMEM (512 columns x 128 lanes, fp32): S_0 [0,128) S_1 [128,256)
-//   O_0 [256,384) O_1 [384,512); P_h (bf16, 64 columns) aliases S_h.
+// TMEM (512 columns x 128 lanes): S [0,128) fp32 (ONE buffer shared by both
+// Q tiles), P_0 [128,192) P_1 [192,256) bf16, O_0 [256,384) O_1 [384,512).
+// A softmax warp releases S right after tcgen05.ld has it in registers, so the
+// next S MMA overlaps the exponentials; P lives in its own columns, and the
+// P.V product lags one KV step.  MMA issue order per step j:
+//     S_0(j)  PV_0(j-1)  S_1(j)  PV_1(j-1)
+// keeping the tensor pipe busy while both softmax warpgroups compute.
+// Correction (O *= 2^(m_old - m_new), only when the running max grows by
+// > 8 in log2 units) runs in the softmax warpgroup after PV_h(j-1) completes
+// and before P_h(j) is published.  The epilogue (O / l, lse) writes HBM
+// straight from registers, so the next Q tile can be loaded as soon as the
+// last S of the current one has been read.
 #include "attention_fwd.h"
 #include "ptx.cuh"
 #include "tma_host.h"
@@ -41,15 +43,17 @@ constexpr int BKV = 128;         // keys per KV tile (S N-extent, PV K-extent)
 constexpr int NSLOT = 5;         // K/V ring slots (32 KiB each)
 constexpr int TILE_BYTES = BKV * D * 2;  // 32 KiB: one Q, K or V tile
 constexpr int HALF_BYTES = TILE_BYTES / 2;  // one 64-column (128-B) swizzle panel
-constexpr int NUM_THREADS = 384;  // 3 warpgroups: softmax 0, softmax 1, {load, MMA, 2 spare}
+constexpr int NUM_THREADS = 384;  // 3 warpgroups
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_KV = 2 * TILE_BYTES;
 constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
+constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);    // P (TMEM) x V (MN-major)
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 256;       // TMEM column bases
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr int kDefaultEmu = 2;  // exp2 pairs (of 8) evaluated on the FMA pipe
+constexpr int HEAD_BAND = 4;    // heads per scheduling band (K/V of a band stays in L2)
 
 struct Params {
   int bh;            // batch * heads
@@ -58,7 +62,9 @@ struct Params {
   int nqb;           // 256-row blocks per head
   float scale_log2;  // scale * log2(e)
   float *lse;        // [bh, seq] or null
+  __nv_bfloat16 *o;  // [bh, seq, 128]
   int scale_pos;     // scale > 0: max on raw scores, scale folded into FFMA2
+  int *work_counter; // dynamic scheduler counter (zeroed before launch)
   unsigned long long *trace;  // optional per-warp cycle accounting [grid][12][8]
 };
 
@@ -70,10 +76,15 @@ __device__ __forceinline__ void kv_range(int r0, const Params &p, int &lo, int &
   hi = last / BKV;
 }
 
+// Work order: bands of HEAD_BAND heads (their K/V stay L2-resident while the
+// band is in flight); inside a band, longest (largest causal q-block) first.
 __device__ __forceinline__ void work_item(int idx, const Params &p, int &bh, int &qb) {
-  // longest-first: largest q-block (most KV tiles under the causal mask) first
-  qb = p.nqb - 1 - idx / p.bh;
-  bh = idx % p.bh;
+  const int per_band = HEAD_BAND * p.nqb;
+  const int band = idx / per_band;
+  const int r = idx - band * per_band;
+  const int heads_in_band = min(HEAD_BAND, p.bh - band * HEAD_BAND);
+  qb = p.nqb - 1 - r / heads_in_band;
+  bh = band * HEAD_BAND + r % heads_in_band;
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -153,8 +164,7 @@ __device__ __forceinline__ uint32_t pack_bf16_2(uint64_t v) {
 template <int EMU>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                     Params p) {
+                     const __grid_constant__ CUtensorMap tmV, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -163,11 +173,15 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   auto q_empty = [&](int h) { return bars + 16 + 8 * h; };
   auto s_full = [&](int h) { return bars + 32 + 8 * h; };
   auto p_full = [&](int h) { return bars + 48 + 8 * h; };
-  auto o_full = [&](int h) { return bars + 64 + 8 * h; };
-  auto kv_full = [&](int s) { return bars + 80 + 8 * s; };
-  auto kv_empty = [&](int s) { return bars + 80 + 8 * NSLOT + 8 * s; };
-  const uint32_t tmem_slot = bars + 80 + 16 * NSLOT;
-  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 80 + 16 * NSLOT);
+  auto o_done = [&](int h) { return bars + 64 + 8 * h; };
+  const uint32_t s_free = bars + 80;
+  auto sched_full = [&](int s) { return bars + 88 + 8 * s; };
+  auto sched_empty = [&](int s) { return bars + 104 + 8 * s; };
+  auto kv_full = [&](int s) { return bars + 120 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 120 + 8 * NSLOT + 8 * s; };
+  const uint32_t tmem_slot = bars + 120 + 16 * NSLOT;
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 120 + 16 * NSLOT);
+  volatile int *sched_slot = reinterpret_cast<int *>(smem + SMEM_BAR + 128 + 16 * NSLOT);  // [2]
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -177,14 +191,16 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    tma_prefetch_desc(&tmO);
     for (int h = 0; h < 2; ++h) {
       mbar_init(q_full(h), 1);
       mbar_init(q_empty(h), 4);
       mbar_init(s_full(h), 1);
       mbar_init(p_full(h), 4);
-      mbar_init(o_full(h), 1);
+      mbar_init(o_done(h), 1);
+      mbar_init(sched_full(h), 1);
+      mbar_init(sched_empty(h), 9);  // MMA thread + 8 softmax warps
     }
+    mbar_init(s_free, 4);
     for (int s = 0; s < NSLOT; ++s) {
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
@@ -198,15 +214,23 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   const uint32_t tmem = *tmem_slot_ptr;
 
   if (warp >= 8) {
-  // control warpgroup gives registers to the two softmax warpgroups
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+  // control warpgroup gives registers to the two softmax warpgroups.  Budget:
+  // the pool only holds what dec releases: 8 warps x (208-168) <= 4 x (168-88).
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
   if (warp == 8) {
-    // ================= TMA producer =================
+    // ================= scheduler + TMA producer =================
     if (lane == 0) {
       int slot = 0;
       uint32_t slot_phase = 0;
       uint32_t qe_phase = 0;
-      for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+      int it = blockIdx.x;
+      for (int n = 0;; ++n) {
+        // publish the work item (or -1) to the consumers
+        const int ss = n & 1;
+        mbar_wait(sched_empty(ss), ((n >> 1) & 1) ^ 1, 12);
+        sched_slot[ss] = it < num_items ? it : -1;
+        mbar_arrive(sched_full(ss));
+        if (it >= num_items) break;
         int bh, qb;
         work_item(it, p, bh, qb);
         const int r0 = qb * 2 * BQ;
@@ -223,7 +247,10 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           tma_load_3d(dq + HALF_BYTES, &tmQ, q_full(h), 64, r0 + h * BQ, bh);
         }
         qe_phase ^= 1;
+        // next item: claimed now so the consumers never wait on the atomic
+        it = atomicAdd(p.work_counter, 1) + (int)gridDim.x;
         for (int j = lo; j <= hi; ++j) {
+#pragma unroll 1
           for (int kv = 0; kv < 2; ++kv) {
             mbar_wait(kv_empty(slot), slot_phase ^ 1, 11);
             mbar_arrive_expect_tx(kv_full(slot), TILE_BYTES);
@@ -238,118 +265,116 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     }
   } else if (warp == 9) {
     // ================= MMA issuer =================
-    if (lane == 0) {
-      int slot = 0;
-      uint32_t slot_phase = 0;
-      uint32_t q_phase = 0;
-      uint32_t p_phase[2] = {0, 0};
-      // Descriptors are rebuilt per MMA from 32-bit pieces (cheap ALU) so the
-      // register-starved control warpgroup does not hoist 64-bit constants.
-      constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO, version, SW128
-      constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;                         // LBO (unused)
-      constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;         // LBO = D-panel stride
-      auto issue_S = [&](int h, uint32_t kslot) {
-        const uint32_t qa = (sbase + SMEM_Q + h * TILE_BYTES) >> 4;
-        const uint32_t kb = (sbase + SMEM_KV + kslot * TILE_BYTES) >> 4;
-        const uint32_t d = tmem + h * 128;
-#pragma unroll 1
+    // The whole warp runs the schedule (so descriptor math stays on the
+    // uniform datapath); one elected lane issues tcgen05.mma / commit.
+    uint32_t ring = 0;  // K/V ring positions consumed so far (K_j at 2(j-lo), V_j at 2(j-lo)+1)
+    uint32_t q_phase = 0, sf_phase = 0;
+    uint32_t p_phase0 = 0, p_phase1 = 0;
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t sb = __shfl_sync(0xffffffffu, sbase, 0);
+    constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO, version, SW128
+    constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;                         // LBO (unused)
+    constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;         // LBO = D-panel stride
+    auto ring_wait = [&](uint32_t pos) { mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 23); };
+    auto issue_S = [&](int h, uint32_t kslot) {
+      mbar_wait(s_free, sf_phase ^ 1, 24);  // S buffer released by its last reader
+      sf_phase ^= 1;
+      tc_fence_after();
+      const uint32_t qa = (sb + SMEM_Q + h * TILE_BYTES) >> 4;
+      const uint32_t kb = (sb + SMEM_KV + kslot * TILE_BYTES) >> 4;
+      if (elect_one()) {
+#pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = ((k >> 2) * HALF_BYTES + (k & 3) * 32) >> 4;
-          mma_f16_ss<1>(d, make_desc(LO_KMAJ | (qa + off), HI_KMAJ), make_desc(LO_KMAJ | (kb + off), HI_KMAJ),
-                        IDESC_S, k != 0);
+          mma_f16_ss<1>(tm + TM_S, make_desc(LO_KMAJ | (qa + off), HI_KMAJ),
+                        make_desc(LO_KMAJ | (kb + off), HI_KMAJ), IDESC_S, k != 0);
         }
         mma_commit(s_full(h));
-      };
-      auto issue_PV = [&](int h, uint32_t vslot, bool acc) {
-        const uint32_t vb = (sbase + SMEM_KV + vslot * TILE_BYTES) >> 4;
-        const uint32_t d = tmem + 256 + h * 128;
-        const uint32_t a = tmem + h * 128;
-#pragma unroll 1
-        for (int k = 0; k < BKV / 16; ++k) {
-          mma_f16_ts<1>(d, a + k * 8, make_desc(LO_VMN | (vb + k * (2048 >> 4)), HI_KMAJ), IDESC_PV,
+      }
+      __syncwarp();
+    };
+    auto issue_PV = [&](int h, uint32_t vslot, bool acc) {
+      mbar_wait(p_full(h), h ? p_phase1 : p_phase0, 25 + h);
+      if (h) p_phase1 ^= 1; else p_phase0 ^= 1;
+      tc_fence_after();
+      const uint32_t vb = (sb + SMEM_KV + vslot * TILE_BYTES) >> 4;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          mma_f16_ts<1>(tm + TM_O + h * 128, tm + TM_P + h * 64 + k * 8,
+                        make_desc(LO_VMN | (vb + k * (2048 >> 4)), HI_KMAJ), IDESC_PV,
                         (acc || k != 0) ? 1u : 0u);
+        mma_commit(o_done(h));
+      }
+      __syncwarp();
+    };
+    auto release = [&](uint32_t slot) {
+      if (elect_one()) mma_commit(kv_empty(slot));
+      __syncwarp();
+    };
+    for (int n = 0;; ++n) {
+      const int ss = n & 1;
+      mbar_wait(sched_full(ss), (n >> 1) & 1, 20);
+      const int it = sched_slot[ss];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sched_empty(ss));
+      if (it < 0) break;
+      int bh, qb;
+      work_item(it, p, bh, qb);
+      const int r0 = qb * 2 * BQ;
+      int lo0, hi0, lo1, hi1;
+      kv_range(r0, p, lo0, hi0);
+      kv_range(r0 + BQ, p, lo1, hi1);
+      const bool has1 = r0 + BQ < p.seq;
+      if (!has1) hi1 = hi0;
+      const int lo = min(lo0, lo1), hi = max(hi0, hi1);
+      mbar_wait(q_full(0), q_phase, 21);
+      mbar_wait(q_full(1), q_phase, 22);
+      q_phase ^= 1;
+      for (int j = lo; j <= hi + 1; ++j) {
+        const uint32_t kpos = ring + 2 * (j - lo);
+        const uint32_t vpos = kpos - 1;  // V_{j-1}
+        if (j <= hi) {
+          ring_wait(kpos);
+          if (j >= lo0 && j <= hi0) issue_S(0, kpos % NSLOT);
         }
-      };
-      long long mt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
-        int bh, qb;
-        work_item(it, p, bh, qb);
-        const int r0 = qb * 2 * BQ;
-        int lo0, hi0, lo1, hi1;
-        kv_range(r0, p, lo0, hi0);
-        kv_range(r0 + BQ, p, lo1, hi1);
-        const bool has1 = r0 + BQ < p.seq;
-        if (!has1) hi1 = hi0;
-        const int lo = min(lo0, lo1), hi = max(hi0, hi1);
-        auto in0 = [&](int j) { return j >= lo0 && j <= hi0; };
-        auto in1 = [&](int j) { return has1 && j >= lo1 && j <= hi1; };
-
-        mbar_wait(q_full(0), q_phase, 20);
-        mbar_wait(q_full(1), q_phase, 21);
-        q_phase ^= 1;
-        tc_fence_after();
-        // prologue: S_h(lo)
-        int kslot = slot;
-        mbar_wait(kv_full(kslot), slot_phase, 22);
-        tc_fence_after();
-        if (in0(lo)) issue_S(0, kslot);
-        if (in1(lo)) issue_S(1, kslot);
-        mma_commit(kv_empty(kslot));
-        if (++slot == NSLOT) { slot = 0; slot_phase ^= 1; }
-        for (int j = lo; j <= hi; ++j) {
-          const int vslot = slot;
-          const long long m2 = p.trace ? clock64() : 0;
-          mbar_wait(kv_full(vslot), slot_phase, 23);
-          if (p.trace) { mt_acc[2] += clock64() - m2; mt_acc[4] += 1; }
-          if (++slot == NSLOT) { slot = 0; slot_phase ^= 1; }
-          int nslot = -1;
-          if (j + 1 <= hi) {
-            nslot = slot;
-            mbar_wait(kv_full(nslot), slot_phase, 24);
-            if (++slot == NSLOT) { slot = 0; slot_phase ^= 1; }
-          }
-          tc_fence_after();
-          if (in0(j)) {
-            const long long m0 = p.trace ? clock64() : 0;
-            mbar_wait(p_full(0), p_phase[0], 25);
-            if (p.trace) mt_acc[0] += clock64() - m0;
-            p_phase[0] ^= 1;
-            tc_fence_after();
-            issue_PV(0, vslot, j != lo0);
-            if (j == hi0) mma_commit(o_full(0));
-          }
-          if (nslot >= 0 && in0(j + 1)) issue_S(0, nslot);
-          if (in1(j)) {
-            const long long m1 = p.trace ? clock64() : 0;
-            mbar_wait(p_full(1), p_phase[1], 26);
-            if (p.trace) mt_acc[1] += clock64() - m1;
-            p_phase[1] ^= 1;
-            tc_fence_after();
-            issue_PV(1, vslot, j != lo1);
-            if (j == hi1) mma_commit(o_full(1));
-          }
-          mma_commit(kv_empty(vslot));
-          if (nslot >= 0) {
-            if (in1(j + 1)) issue_S(1, nslot);
-            mma_commit(kv_empty(nslot));
-          }
+        if (j > lo) {
+          ring_wait(vpos);
+          if (j - 1 >= lo0 && j - 1 <= hi0) issue_PV(0, vpos % NSLOT, j - 1 != lo0);
+        }
+        if (j <= hi) {
+          if (has1 && j >= lo1 && j <= hi1) issue_S(1, kpos % NSLOT);
+          release(kpos % NSLOT);  // K_j: both S products issued
+        }
+        if (j > lo) {
+          if (has1 && j - 1 >= lo1 && j - 1 <= hi1) issue_PV(1, vpos % NSLOT, j - 1 != lo1);
+          release(vpos % NSLOT);  // V_{j-1}
         }
       }
-      if (p.trace)
-        for (int e = 0; e < 8; ++e) p.trace[((size_t)blockIdx.x * 12 + warp) * 8 + e] = mt_acc[e];
+      ring += 2 * (hi - lo + 1);
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     // ================= softmax / correction / epilogue (WG h) =================
     const int h = warp >> 2;             // Q tile owned by this warpgroup
     const int q = warp & 3;              // TMEM lane quarter
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const uint32_t t_s = tmem + t_lane + h * 128;
-    const uint32_t t_o = tmem + t_lane + 256 + h * 128;
-    uint32_t s_phase = 0, o_phase = 0;
+    const uint32_t t_s = tmem + t_lane + TM_S;
+    const uint32_t t_p = tmem + t_lane + TM_P + h * 64;
+    const uint32_t t_o = tmem + t_lane + TM_O + h * 128;
+    uint32_t s_phase = 0;
+    uint32_t od_count = 0;  // o_done[h] phases consumed (one per PV_h)
+#ifdef MIMW_FA_TRACE
     long long tr_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+#endif
+    for (int n = 0;; ++n) {
+      const int ss = n & 1;
+      mbar_wait(sched_full(ss), (n >> 1) & 1, 28);
+      const int it = sched_slot[ss];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sched_empty(ss));
+      if (it < 0) break;
       int bh, qb;
       work_item(it, p, bh, qb);
       const int rt = qb * 2 * BQ + h * BQ;  // first row of this Q tile
@@ -359,159 +384,168 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       kv_range(rt, p, lo, hi);
       float m_used = -INFINITY;  // log2-domain max the exponentials are taken against
       float l = 0.f;
-      if (tile_live) {
-        for (int j = lo; j <= hi; ++j) {
-          const long long tr0 = p.trace ? clock64() : 0;
-          mbar_wait(s_full(h), s_phase, 30 + h);
-          s_phase ^= 1;
-          tc_fence_after();
-          const long long tr1 = p.trace ? clock64() : 0;
-          uint32_t s[128];
-          tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-          tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-          tmem_ld_32x32b_x32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-          tmem_ld_32x32b_x32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
-          tmem_ld_wait();
-          const long long tr2 = p.trace ? clock64() : 0;
-          const int k0 = j * BKV;
-          if (!p.scale_pos) {
-            // non-positive scale: move to the log2 domain first (max must see scaled values)
-#pragma unroll
-            for (int c = 0; c < 128; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
-          }
-          // tile needs masking if any (row, key) pair of the whole Q tile is invalid
-          const bool need_mask = (k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window) ||
-                                 (k0 + BKV > p.seq);
-          if (need_mask) {
-            // valid keys of this row form one contiguous column range [c_lo, c_hi]
-            const int c_lo = row - p.window + 1 - k0;
-            const int c_hi = min(row, p.seq - 1) - k0;
-#pragma unroll
-            for (int c = 0; c < 128; ++c)
-              if (c < c_lo || c > c_hi) s[c] = 0xff800000u;  // -inf
-          }
-          // row max: four independent 3-input max chains
-          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-          for (int c = 0; c < 128; c += 8) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
-          }
-          const float sl = p.scale_pos ? p.scale_log2 : 1.f;
-          const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
-          // online softmax: only move the reference max when it grows by > 8
-          // (2^8 headroom in fp32 / bf16 P), which makes O rescales rare.
-          float corr = 1.f;
-          bool rescale = false;
-          if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-            corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
-            rescale = (j != lo);
-            m_used = mx;
-          }
-          l *= corr;
-          const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
-          const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
-          uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {  // 16 keys per group -> 8 packed P columns
-            uint32_t pk[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int c = g * 16 + 2 * e;
-              // x = s * scale*log2e - m, two lanes per FFMA2
-              const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
-              const uint64_t p2 = (e < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
-              acc[e & 3] = f2_add(acc[e & 3], p2);
-              pk[e] = pack_bf16_2(p2);
-            }
-            // P_h(j) -> TMEM (aliases S_h columns [0, 64)); S is already in registers
-            tmem_st_32x32b_x8(t_s + g * 8, pk);
-          }
-          {
-            float a0, a1, b0, b1, c0, c1, d0, d1;
-            f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-            f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-            (void)c0; (void)c1; (void)d0; (void)d1;
-            l += (a0 + a1) + (b0 + b1);
-          }
-          // correction: O_h (complete through PV_h(j-1)) *= corr for rows whose max moved
-          if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll 1
-            for (int c = 0; c < 128; c += 32) {
-              uint32_t o[32];
-              tmem_ld_32x32b_x32(t_o + c, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-              tmem_st_32x32b_x16(t_o + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
-              tmem_st_32x32b_x16(t_o + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
-            }
-          }
-          const long long tr3 = p.trace ? clock64() : 0;
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(p_full(h));
-          if (p.trace) {
-            tr_acc[0] += tr1 - tr0;  // waiting for S
-            tr_acc[1] += tr2 - tr1;  // TMEM load of S
-            tr_acc[2] += tr3 - tr2;  // max / exp2 / P store issue (+ rare O rescale)
-            tr_acc[3] += clock64() - tr3;  // st wait + arrive
-            tr_acc[4] += 1;
-          }
-        }
+      if (!tile_live) {
+        if (lane == 0) mbar_arrive(q_empty(h));
+        continue;
       }
-      // ---------------- epilogue: O / l, lse ----------------
-      // (always arrive q_empty so the producer's phase accounting stays aligned)
-      if (tile_live) {
-        mbar_wait(o_full(h), o_phase, 40 + h);
+      for (int j = lo; j <= hi; ++j) {
+#ifdef MIMW_FA_TRACE
+        const long long tr0 = clock64();
+#endif
+        mbar_wait(s_full(h), s_phase, 30 + h);
+        s_phase ^= 1;
         tc_fence_after();
-      }
-      o_phase ^= tile_live ? 1 : 0;
-      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
-      if (tile_live && p.lse != nullptr && row < p.seq)
-        p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(l)) * (1.0f / LOG2E);
-      const uint32_t qbuf = sbase + SMEM_Q + h * TILE_BYTES;
-      if (tile_live) {
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-          // rows of this warp: 32 x 128 B in panel `half`; SWIZZLE_128B chunk c at c ^ (r & 7)
-          const uint32_t wbuf = qbuf + half * HALF_BYTES + q * 32 * 128;
+#ifdef MIMW_FA_TRACE
+        const long long tr1 = clock64();
+#endif
+        uint32_t s[128];
+        tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld_32x32b_x32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+        tmem_ld_32x32b_x32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        tmem_ld_wait();
+        // S is in registers: hand the buffer back (and Q_h after its last S)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(s_free);
+          if (j == hi) mbar_arrive(q_empty(h));
+        }
+#ifdef MIMW_FA_TRACE
+        const long long tr2 = clock64();
+#endif
+        const int k0 = j * BKV;
+        if (!p.scale_pos) {
+          // non-positive scale: move to the log2 domain first (max must see scaled values)
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
+          for (int c = 0; c < 128; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
+        }
+        // tile needs masking if any (row, key) pair of the whole Q tile is invalid
+        const bool need_mask = (k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window) ||
+                               (k0 + BKV > p.seq);
+        if (need_mask) {
+          // valid keys of this row form one contiguous column range [c_lo, c_hi]
+          const int c_lo = row - p.window + 1 - k0;
+          const int c_hi = min(row, p.seq - 1) - k0;
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c < c_lo || c > c_hi) s[c] = 0xff800000u;  // -inf
+        }
+        // row max: four independent 3-input max chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
+        }
+        const float sl = p.scale_pos ? p.scale_log2 : 1.f;
+        const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
+        // online softmax: only move the reference max when it grows by > 8
+        // (2^8 headroom in fp32 / bf16 P), which makes O rescales rare.
+        float corr = 1.f;
+        bool rescale = false;
+        if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
+          corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
+          rescale = (j != lo);
+          m_used = mx;
+        }
+        l *= corr;
+        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
+        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
+        uint64_t acc[4] = {0, 0, 0, 0};
+        uint32_t pk[64];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const int c = 2 * e;
+          // x = s * scale*log2e - m, two lanes per FFMA2
+          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
+          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
+          acc[e & 3] = f2_add(acc[e & 3], p2);
+          pk[e] = pack_bf16_2(p2);
+        }
+        {
+          float a0, a1, b0, b1;
+          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
+          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
+          l += (a0 + a1) + (b0 + b1);
+        }
+#ifdef MIMW_FA_TRACE
+        const long long tr3 = clock64();
+#endif
+        // PV_h(j-1) must be complete before P_h is overwritten / O_h rescaled.
+        // o_done[h] can be at most one phase ahead of the one awaited here
+        // (PV_h(j) needs this P), so the parity wait is unambiguous.
+        if (j > lo) {
+          mbar_wait(o_done(h), od_count & 1, 32 + h);
+          ++od_count;
+          tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+          for (int c = 0; c < 128; c += 32) {
             uint32_t o[32];
-            tmem_ld_32x32b_x32(t_o + half * 64 + c2 * 32, o);
+            tmem_ld_32x32b_x32(t_o + c, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint32_t chunk = (uint32_t)(c2 * 4 + c) ^ (lane & 7);
-              st_shared_v4(wbuf + lane * 128 + chunk * 16,
-                           pack_bf16(__uint_as_float(o[8 * c + 0]) * inv_l, __uint_as_float(o[8 * c + 1]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * c + 2]) * inv_l, __uint_as_float(o[8 * c + 3]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * c + 4]) * inv_l, __uint_as_float(o[8 * c + 5]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * c + 6]) * inv_l, __uint_as_float(o[8 * c + 7]) * inv_l));
-            }
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x16(t_o + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
+            tmem_st_32x32b_x16(t_o + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
           }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&tmO, wbuf, half * 64, rt + q * 32, bh);
-            bulk_commit();
+        }
+#ifdef MIMW_FA_TRACE
+        const long long tr4 = clock64();
+#endif
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          tmem_st_32x32b_x16(t_p + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[g * 16]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full(h));
+#ifdef MIMW_FA_TRACE
+        {
+          tr_acc[0] += tr1 - tr0;  // waiting for S
+          tr_acc[1] += tr2 - tr1;  // TMEM load of S
+          tr_acc[2] += tr3 - tr2;  // max / exp2 (registers)
+          tr_acc[3] += tr4 - tr3;  // wait PV_h(j-1) + rare O rescale
+          tr_acc[5] += clock64() - tr4;  // P store + arrive
+          tr_acc[4] += 1;
+        }
+#endif
+      }
+      // ---------------- epilogue: O / l, lse, straight to HBM ----------------
+      mbar_wait(o_done(h), od_count & 1, 40 + h);
+      ++od_count;
+      tc_fence_after();
+      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+      if (row < p.seq) {
+        if (p.lse != nullptr) p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(l)) * (1.0f / LOG2E);
+      }
+      uint4 *orow = reinterpret_cast<uint4 *>(p.o + ((size_t)bh * p.seq + row) * D);
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(t_o + c, o);
+        tmem_ld_wait();
+        if (row < p.seq) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l);
+            w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l);
+            w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l);
+            w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l);
+            orow[c / 8 + v] = w;
           }
         }
       }
-      tc_fence_before();
-      if (lane == 0) {
-        bulk_wait_read<0>();
-        mbar_arrive(q_empty(h));
-      }
-      __syncwarp();
+      tc_fence_before();  // O_h read before the next item's first PV_h overwrites it
     }
+#ifdef MIMW_FA_TRACE
     if (p.trace && lane == 0)
       for (int e = 0; e < 8; ++e) p.trace[((size_t)blockIdx.x * 12 + warp) * 8 + e] = tr_acc[e];
-    if (lane == 0) bulk_wait<0>();
-    __syncwarp();
+#endif
   }
 
   tc_fence_before();
@@ -524,6 +558,16 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 
 }  // namespace
 
+// per-device scheduler counters (zeroed on the launch stream before every launch)
+static int *work_counter(int device) {
+  static int *ctr[64] = {nullptr};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!ctr[device]) {
+    if (cudaMalloc(&ctr[device], sizeof(int)) != cudaSuccess) return nullptr;
+  }
+  return ctr[device];
+}
+
 cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   const uint64_t bh = (uint64_t)a.batch * a.heads;
   CUtensorMap tQ = make_tmap_3d(a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
@@ -532,8 +576,6 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tV = make_tmap_3d(a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  CUtensorMap tO = make_tmap_3d(a.o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
-                                (uint64_t)a.seq * D, 64, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   Params p;
   p.bh = (int)bh;
   p.seq = (int)a.seq;
@@ -541,16 +583,23 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   p.nqb = (int)((a.seq + 2 * BQ - 1) / (2 * BQ));
   p.scale_log2 = (float)(a.scale * 1.4426950408889634);
   p.lse = a.lse;
+  p.o = static_cast<__nv_bfloat16 *>(a.o);
   p.trace = a.trace;
+  p.scale_pos = a.scale > 0 ? 1 : 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  p.work_counter = work_counter(dev);
+  if (!p.work_counter) return cudaErrorMemoryAllocation;
   const int items = p.bh * p.nqb;
   int grid = sm_count();
   if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
   if (grid > items) grid = items;
-  p.scale_pos = a.scale > 0 ? 1 : 0;
+  cudaError_t e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
   auto launch = [&](auto kern) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, tO, p);
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, p);
     return cudaGetLastError();
   };
   switch (a.emu < 0 ? kDefaultEmu : a.emu) {

@@ -20,6 +20,10 @@
 // sim.cpp:1500-1555).  ~8 s at 1.9 GHz.
 #define MIMW_WATCHDOG_CYCLES (16ull << 30)
 #endif
+#ifdef MIMW_WATCHDOG_PRINTF
+#undef MIMW_WATCHDOG_CYCLES
+#define MIMW_WATCHDOG_CYCLES (1ull << 31)
+#endif
 
 namespace mimw {
 
@@ -126,6 +130,10 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
 __device__ uint32_t g_mimw_watchdog[4];
 
 static __device__ __forceinline__ void watchdog_trap(uint32_t bar, uint32_t parity, int tag) {
+#ifdef MIMW_WATCHDOG_PRINTF  // debug builds only: the call perturbs register allocation
+  printf("mimw watchdog: block %d thread %d stuck on mbarrier 0x%x parity %u tag %d\n", blockIdx.x,
+         threadIdx.x, bar, parity, tag);
+#endif
   g_mimw_watchdog[0] = 1u;
   g_mimw_watchdog[1] = bar;
   g_mimw_watchdog[2] = parity;

@@ -35,7 +35,7 @@ mma = t[:, 9, :].mean(dim=0)
 n = sm[4].item()
 print(f"kernel {ms:.3f} ms (traced)")
 print(f"softmax warp per tile (n={n:.0f}/warp): wait_S {sm[0]/n:.0f}  ld_S {sm[1]/n:.0f}  "
-      f"compute {sm[2]/n:.0f}  st_wait+arrive {sm[3]/n:.0f} cycles")
+      f"max+exp {sm[2]/n:.0f}  wait_PV+rescale {sm[3]/n:.0f}  P store+arrive {sm[5]/n:.0f} cycles")
 nm = mma[4].item()
 print(f"MMA warp per KV step (n={nm:.0f}): wait_P0 {mma[0]/nm:.0f}  wait_P1 {mma[1]/nm:.0f}  "
-      f"wait_V {mma[2]/nm:.0f} cycles")
+      f"wait_K {mma[2]/nm:.0f}  wait_Sfree {mma[3]/nm:.0f} cycles")

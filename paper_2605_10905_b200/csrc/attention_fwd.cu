@@ -399,10 +399,25 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         const long long tr1 = clock64();
 #endif
         uint32_t s[128];
+        // two halves: the second pair of loads overlaps the first half's max
         tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld_wait();
         tmem_ld_32x32b_x32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
         tmem_ld_32x32b_x32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        const int k0 = j * BKV;
+        // tile needs masking if any (row, key) pair of the whole Q tile is invalid
+        const bool need_mask = (k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window) ||
+                               (k0 + BKV > p.seq) || !p.scale_pos;
+        if (!need_mask) {
+#pragma unroll
+          for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
+          }
+        }
         tmem_ld_wait();
         // S is in registers: hand the buffer back (and Q_h after its last S)
         tc_fence_before();
@@ -414,27 +429,28 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 #ifdef MIMW_FA_TRACE
         const long long tr2 = clock64();
 #endif
-        const int k0 = j * BKV;
-        if (!p.scale_pos) {
-          // non-positive scale: move to the log2 domain first (max must see scaled values)
-#pragma unroll
-          for (int c = 0; c < 128; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
-        }
-        // tile needs masking if any (row, key) pair of the whole Q tile is invalid
-        const bool need_mask = (k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window) ||
-                               (k0 + BKV > p.seq);
         if (need_mask) {
+          if (!p.scale_pos) {
+            // non-positive scale: move to the log2 domain first (max must see scaled values)
+#pragma unroll
+            for (int c = 0; c < 128; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
+          }
           // valid keys of this row form one contiguous column range [c_lo, c_hi]
           const int c_lo = row - p.window + 1 - k0;
           const int c_hi = min(row, p.seq - 1) - k0;
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c < c_lo || c > c_hi) s[c] = 0xff800000u;  // -inf
-        }
-        // row max: four independent 3-input max chains
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 128; c += 8) {
+          for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
+          }
+        }
+        // row max over the second half: four independent 3-input max chains
+#pragma unroll
+        for (int c = 64; c < 128; c += 8) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
@@ -451,25 +467,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           m_used = mx;
         }
         l *= corr;
-        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
-        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
-        uint64_t acc[4] = {0, 0, 0, 0};
-        uint32_t pk[64];
-#pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const int c = 2 * e;
-          // x = s * scale*log2e - m, two lanes per FFMA2
-          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
-          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
-          acc[e & 3] = f2_add(acc[e & 3], p2);
-          pk[e] = pack_bf16_2(p2);
-        }
-        {
-          float a0, a1, b0, b1;
-          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-          l += (a0 + a1) + (b0 + b1);
-        }
 #ifdef MIMW_FA_TRACE
         const long long tr3 = clock64();
 #endif
@@ -496,9 +493,28 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 #ifdef MIMW_FA_TRACE
         const long long tr4 = clock64();
 #endif
+        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
+        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
+        uint64_t acc[4] = {0, 0, 0, 0};
+        uint32_t pk[64];
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          tmem_st_32x32b_x16(t_p + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[g * 16]));
+        for (int e = 0; e < 64; ++e) {
+          const int c = 2 * e;
+          // x = s * scale*log2e - m, two lanes per FFMA2
+          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
+          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
+          acc[e & 3] = f2_add(acc[e & 3], p2);
+          pk[e] = pack_bf16_2(p2);
+          // stream P_h(j) into TMEM 16 columns (32 keys) at a time
+          if ((e & 15) == 15)
+            tmem_st_32x32b_x16(t_p + (e - 15), *reinterpret_cast<uint32_t(*)[16]>(&pk[e - 15]));
+        }
+        {
+          float a0, a1, b0, b1;
+          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
+          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
+          l += (a0 + a1) + (b0 + b1);
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -507,9 +523,9 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         {
           tr_acc[0] += tr1 - tr0;  // waiting for S
           tr_acc[1] += tr2 - tr1;  // TMEM load of S
-          tr_acc[2] += tr3 - tr2;  // max / exp2 (registers)
+          tr_acc[2] += tr3 - tr2;  // max + online-softmax bookkeeping
           tr_acc[3] += tr4 - tr3;  // wait PV_h(j-1) + rare O rescale
-          tr_acc[5] += clock64() - tr4;  // P store + arrive
+          tr_acc[5] += clock64() - tr4;  // exp2 + streamed P store + arrive
           tr_acc[4] += 1;
         }
 #endif

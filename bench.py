@@ -354,13 +354,65 @@ def bench_attention(args, rank, ws, local):
     return res
 
 
+def bench_mxfp8(args, rank, ws, local):
+    """configs[2]: FP8 (e4m3) block-scaled GEMM M=N=K=8192 (MXFP8, UE8M0 per
+    1x32 along K), one independent GEMM per GPU (weak scaling)."""
+    import torch
+    import paper_2605_10905_b200 as P
+    L = P.lib()
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev).manual_seed(3 + rank)
+    m = n = k = GEMM_M
+    qa = torch.randint(0, 256, (m, k), device=dev, dtype=torch.uint8, generator=g)
+    qb = torch.randint(0, 256, (n, k), device=dev, dtype=torch.uint8, generator=g)
+    qa[(qa & 0x7F) == 0x7F] = 0x38
+    qb[(qb & 0x7F) == 0x7F] = 0x38
+    sfa = torch.randint(120, 134, (m, k // 32), device=dev, dtype=torch.uint8, generator=g)
+    sfb = torch.randint(120, 134, (n, k // 32), device=dev, dtype=torch.uint8, generator=g)
+    c = torch.empty((m, n), device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def step():
+        P._check(L.mimw_b200_gemm_mxfp8(qa.data_ptr(), sfa.data_ptr(), qb.data_ptr(), sfb.data_ptr(),
+                                        c.data_ptr(), m, n, k, sptr))
+
+    steps = args.steps
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(step, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    flop = 2.0 * m * n * k
+    achieved = flop / (secs / steps) / 1e12
+    # cuBLAS FP8 (torch._scaled_mm, per-tensor scales) on the same box as a reference point
+    ref = None
+    try:
+        a8 = qa.view(torch.float8_e4m3fn)
+        b8 = qb.view(torch.float8_e4m3fn)
+        one = torch.ones((), device=dev)
+        f = lambda: torch._scaled_mm(a8, b8.t(), scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        rs = timed(f, 10, 3, 1, stream)
+        ref = round(flop * 10 / rs / 1e12, 1)
+    except Exception as e:  # noqa: BLE001
+        ref = f"unavailable: {type(e).__name__}"
+    return {"value": round(ws * flop * steps / secs / 1e12, 2), "unit": "TFLOPS",
+            "ms_per_step": round(secs / steps * 1e3, 4), "scaling": "weak",
+            "config": {"workload": "configs[2]: MXFP8 e4m3 block-scaled GEMM M=N=K=8192 "
+                                   "(UE8M0 per 1x32 along K), bf16 out, 128x224x128 tiles"},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": 4500.0,
+                         "unit": "TFLOP/s", "frac": round(achieved / 4500.0, 4),
+                         "peak_source": "spec dense FP8 (no measured FP8 peak in MEASURED_PEAKS.json)",
+                         "cublas_fp8_scaled_mm_tflops_same_box": ref, "traffic": None},
+            "clocks": clocks}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention"])
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -398,12 +450,15 @@ def main():
     rank, ws, local = dist_init(args.gpus)
     if args.workload == "attention":
         res = bench_attention(args, rank, ws, local)
+    elif args.workload == "fp8":
+        res = bench_mxfp8(args, rank, ws, local)
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
             fa = bench_attention(args, rank, ws, local)
             res["secondary"] = {"attention_fwd": {k: fa[k] for k in (
                 "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks")}}
+            res["secondary"]["mxfp8_gemm"] = bench_mxfp8(args, rank, ws, local)
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

@@ -66,6 +66,16 @@ int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_
                         int64_t lda, int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype,
                         void *stream);
 
+/* ---- Block-scaled FP8 GEMM (MXFP8) -----------------------------------------
+ * C[m,n] (bf16) = sum_k e4m3(a[m,k]) 2^(sfa[m,k/32]-127) * e4m3(b[n,k]) 2^(sfb[n,k/32]-127)
+ * No reference counterpart; its oracle is oracle_gemm
+ * (oracles.cpp:14-26) on the dequantised Tiles.  Device buffers: a e4m3
+ * [m,k], b e4m3 [n,k] (both K-contiguous), sfa ue8m0 [m,k/32], sfb ue8m0
+ * [n,k/32], c bf16 [m,n]; k % 32 == 0.  tcgen05.mma.kind::mxf8f6f4.block_scale
+ * with scale factors staged smem->TMEM by tcgen05.cp. */
+int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
+                         int64_t m, int64_t n, int64_t k, void *stream);
+
 /* ---- K-gathered GEMM: C = [a0 | a1] . [b0 ; b1] ---------------------------
  * Replaces: Tile oracle_multi_device_gemm(a0, a1, b0, b1)
  *           oracles.hpp:24-25 (oracles.cpp:57-80).  Host f32 buffers. */

@@ -18,6 +18,7 @@
 #include "convert.h"
 #include "attention_fwd.h"
 #include "gemm_bf16.h"
+#include "gemm_mxfp8.h"
 
 namespace {
 
@@ -307,6 +308,43 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
     a.window = window;
     a.scale = scale;
     check_cuda(mimw::attention_fwd_launch(a, static_cast<cudaStream_t>(stream)), "attention launch");
+  });
+}
+
+int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
+                         int64_t m, int64_t n, int64_t k, void *stream) {
+  return guarded([&] {
+    require(m >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
+    require(k % 32 == 0, MIMW_ERR_SHAPE, "k must be a multiple of the 32-element scale block");
+    require(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
+    if (m == 0 || n == 0) return;
+    require(c != nullptr, MIMW_ERR_ARG, "null pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (k == 0) {
+      require_sm100();
+      check_cuda(cudaMemsetAsync(c, 0, (size_t)m * n * 2, s), "memset");
+      return;
+    }
+    require(a && b && sfa && sfb, MIMW_ERR_ARG, "null pointer");
+    require_pitch(a, k, 1, "a");
+    require_pitch(b, k, 1, "b");
+    require_pitch(c, n, 2, "c");
+    require_sm100();
+    DevBuf ws(mimw::gemm_mxfp8_workspace(m, n, k), s);
+    mimw::Mxfp8Args g{};
+    g.a = a;
+    g.sfa = sfa;
+    g.b = b;
+    g.sfb = sfb;
+    g.c = c;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.lda = k;
+    g.ldb = k;
+    g.ldc = n;
+    g.workspace = ws.p;
+    check_cuda(mimw::gemm_mxfp8_launch(g, s), "mxfp8 gemm launch");
   });
 }
 

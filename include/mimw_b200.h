@@ -76,6 +76,20 @@ int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_
 int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
                          int64_t m, int64_t n, int64_t k, void *stream);
 
+/* ---- Grouped (MoE) GEMM ---------------------------------------------------
+ * For every group (expert) e < n_groups:
+ *   y[m_offsets[e] : m_offsets[e+1], :] = x[m_offsets[e] : m_offsets[e+1], :] . W_e
+ * No reference counterpart; its oracle is one
+ * oracle_gemm (oracles.cpp:14-26) per group.  x bf16 [m_offsets[G], k] and
+ * y bf16 [m_offsets[G], n] are DEVICE buffers with rows packed by group;
+ * m_offsets is a HOST int64 array of n_groups + 1 non-decreasing row offsets
+ * (empty groups allowed); w bf16 is [G, k, n] (MIMW_B_KN, the reference's
+ * B layout) or [G, n, k] (MIMW_B_NK).  n and k multiples of 8.  Persistent
+ * 2-CTA kernel; each group's tail tile is clipped by its own Y tensor map. */
+int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const void *w, void *y,
+                                int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
+                                void *stream);
+
 /* ---- K-gathered GEMM: C = [a0 | a1] . [b0 ; b1] ---------------------------
  * Replaces: Tile oracle_multi_device_gemm(a0, a1, b0, b1)
  *           oracles.hpp:24-25 (oracles.cpp:57-80).  Host f32 buffers. */

@@ -166,6 +166,24 @@ def oracle_gemm(a, b, rows=None) -> np.ndarray:
     return full[r0:r1]
 
 
+def oracle_grouped_gemm(x, m_offsets, w, rows=None) -> list:
+    """Grouped (MoE) GEMM oracle: one ``oracle_gemm`` (oracles.cpp:14-26) per
+    group, ``Y_e = X[off_e:off_e+1] . W_e`` with W as [G, K, N].  The
+    reference has no grouped GEMM (parity anchored on
+    oracle_gemm).  ``rows`` = optional {e: (r0, r1)} row ranges (exact)."""
+    out = []
+    for e in range(len(m_offsets) - 1):
+        xe = x[m_offsets[e]:m_offsets[e + 1]]
+        if rows is not None:
+            if e not in rows:
+                out.append(None)
+                continue
+            out.append(oracle_gemm(xe, w[e], rows=rows[e]))
+        else:
+            out.append(oracle_gemm(xe, w[e]) if len(xe) else np.zeros((0, w.shape[2]), np.float32))
+    return out
+
+
 def oracle_multi_device_gemm(a0, a1, b0, b1) -> np.ndarray:
     a0, a1, b0, b1 = map(_f32, (a0, a1, b0, b1))
     m, k0 = a0.shape

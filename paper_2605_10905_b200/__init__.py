@@ -75,6 +75,8 @@ def _optional_sigs():
                                                                            C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
+        "mimw_b200_grouped_gemm_bf16_ex": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32,
+                                           C.c_int32, C.c_int32, _vp],
     }
 
 
@@ -214,4 +216,31 @@ def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None):
         out = torch.empty((m, n), device=a.device, dtype=torch.bfloat16)
     _check(lib().mimw_b200_gemm_mxfp8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), sfb.data_ptr(),
                                       out.data_ptr(), m, n, k, _stream(stream)))
+    return out
+
+
+def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, cta_group: int = 2,
+                 max_clusters: int = 0):
+    """Grouped (MoE) GEMM: for each group e, ``out[off[e]:off[e+1]] =
+    x[off[e]:off[e+1]] @ W_e`` with bf16 x [rows, K], w [G, K, N] (B_KN) or
+    [G, N, K] (B_NK) CUDA tensors and ``m_offsets`` a host sequence of G+1
+    non-decreasing row offsets.  Returns bf16 [rows, N]."""
+    import torch
+    offs = np.ascontiguousarray(np.asarray(m_offsets, dtype=np.int64))
+    g = w.shape[0]
+    if offs.shape != (g + 1,):
+        raise MimwError(ERR_SHAPE, f"m_offsets must have n_groups + 1 = {g + 1} entries")
+    n, k = (w.shape[2], w.shape[1]) if w_layout == B_KN else (w.shape[1], w.shape[2])
+    if x.shape[1] != k:
+        raise MimwError(ERR_SHAPE, f"dot conformance: x.shape[1]={x.shape[1]} != K={k}")
+    if x.shape[0] < offs[-1]:
+        raise MimwError(ERR_SHAPE, "x has fewer rows than m_offsets[-1]")
+    for t in (x, w):
+        if not t.is_contiguous():
+            raise MimwError(ERR_UNSUPPORTED, "grouped_gemm needs contiguous tensors")
+    if out is None:
+        out = torch.empty((x.shape[0], n), device=x.device, dtype=torch.bfloat16)
+    _check(lib().mimw_b200_grouped_gemm_bf16_ex(x.data_ptr(), offs.ctypes.data, w.data_ptr(),
+                                                out.data_ptr(), g, n, k, w_layout, cta_group,
+                                                max_clusters, _stream(stream)))
     return out

@@ -219,6 +219,40 @@ void host_attention(const float *q, const float *k, const float *v, float *o, fl
   check_cuda(cudaStreamSynchronize(s), "attention execution");
 }
 
+void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *y, int64_t n_groups,
+                  int64_t n, int64_t k, int32_t w_layout, int cta_group, int max_clusters,
+                  cudaStream_t stream) {
+  require(w_layout == MIMW_B_KN || w_layout == MIMW_B_NK, MIMW_ERR_ARG, "bad w_layout");
+  require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
+  require(n_groups >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
+  if (n_groups == 0 || n == 0) return;
+  require(m_offsets != nullptr, MIMW_ERR_ARG, "null m_offsets");
+  require(m_offsets[0] >= 0, MIMW_ERR_SHAPE, "m_offsets[0] < 0");
+  for (int64_t e = 0; e < n_groups; ++e)
+    require(m_offsets[e + 1] >= m_offsets[e], MIMW_ERR_SHAPE, "m_offsets must be non-decreasing");
+  require(m_offsets[n_groups] < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31),
+          MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
+  if (m_offsets[n_groups] == m_offsets[0]) return;
+  require(y != nullptr && (k == 0 || (x && w)), MIMW_ERR_ARG, "null pointer");
+  require(n % 8 == 0 && k % 8 == 0, MIMW_ERR_UNSUPPORTED,
+          "grouped GEMM needs n and k multiples of 8 (16-byte TMA row pitch)");
+  require((((uintptr_t)x | (uintptr_t)w | (uintptr_t)y) & 15) == 0, MIMW_ERR_UNSUPPORTED,
+          "tensors must be 16-byte aligned");
+  require_sm100();
+  mimw::GroupedGemmArgs g{};
+  g.x = x;
+  g.m_offsets = m_offsets;
+  g.w = w;
+  g.y = y;
+  g.n_groups = n_groups;
+  g.n = n;
+  g.k = k;
+  g.w_kn = w_layout == MIMW_B_KN;
+  g.cta_group = cta_group;
+  g.max_clusters = max_clusters;
+  check_cuda(mimw::grouped_gemm_bf16_launch(g, stream), "grouped gemm launch");
+}
+
 }  // namespace
 
 extern "C" {
@@ -345,6 +379,25 @@ int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const vo
     g.ldc = n;
     g.workspace = ws.p;
     check_cuda(mimw::gemm_mxfp8_launch(g, s), "mxfp8 gemm launch");
+  });
+}
+
+int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const void *w, void *y,
+                                int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
+                                void *stream) {
+  return guarded([&] {
+    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Test hook (not part of the public header): grouped GEMM with forced
+// cta_group / cluster cap.
+int mimw_b200_grouped_gemm_bf16_ex(const void *x, const int64_t *m_offsets, const void *w, void *y,
+                                   int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
+                                   int32_t cta_group, int32_t max_clusters, void *stream) {
+  return guarded([&] {
+    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, cta_group, max_clusters,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -31,6 +31,9 @@
 #include "ptx.cuh"
 #include "tma_host.h"
 
+#include <algorithm>
+#include <cstring>
+
 namespace mimw {
 
 namespace {
@@ -58,24 +61,78 @@ struct Cfg {
   static constexpr uint32_t IDESC = idesc_bf16(BM_CTA * CG, BN, 0, B_MN ? 1 : 0);
 };
 
+// One output tile of a (possibly grouped) problem.  Row `mt * BM` of the
+// group starts at A row `row_base + mt * BM`; rows at or beyond `rows` are
+// not stored (C/Y map row extent).
+struct TileCoord {
+  int e, mt, nt, row_base, rows;
+};
+
+// Dense problem: one [M,K] x B -> [M,N]; grouped-rasterised tile order
+// (`group` M-tiles share each N sweep so B panels are re-read from L2).
 struct Sched {
-  int num_m, num_n, group;
-  __device__ __forceinline__ void tile(int t, int &mt, int &nt) const {
+  static constexpr bool kGrouped = false;
+  int num_m, num_n, group, M;
+  __device__ __forceinline__ int num_tiles() const { return num_m * num_n; }
+  __device__ __forceinline__ TileCoord decode(int t) const {
     int per_group = group * num_n;
     int g = t / per_group;
     int first_m = g * group;
     int gsize = min(num_m - first_m, group);
     int r = t - g * per_group;
-    mt = first_m + r % gsize;
-    nt = r / gsize;
+    TileCoord c;
+    c.e = 0;
+    c.mt = first_m + r % gsize;
+    c.nt = r / gsize;
+    c.row_base = 0;
+    c.rows = M;
+    return c;
   }
+  __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *tmC, int) const { return tmC; }
 };
 
-template <int CG, bool B_MN, typename OutT>
+// Grouped (MoE) problem: Y_e[m_e, N] = X[row_off_e : row_off_e + m_e, K] . W_e
+// for e < n_groups.  X rows are packed by group; W is one [G, K, N] (or
+// [G, N, K]) tensor read through a 3-D tensor map; every group has its own
+// Y tensor map whose row extent m_e clips the tail tile's store.  Tile order:
+// groups in turn, N-tiles outer, M-tiles inner, so the CTA pairs working on
+// one weight panel W_e[:, n-tile] run at the same time and share it in L2.
+constexpr int MAX_GROUPS = 128;
+struct GroupedSched {
+  static constexpr bool kGrouped = true;
+  CUtensorMap y[MAX_GROUPS];
+  int tile_off[MAX_GROUPS + 1];  // prefix sum of m_tiles(e) * num_n
+  int row_off[MAX_GROUPS];       // first row of group e in X / Y
+  int rows[MAX_GROUPS];          // m_e
+  int n_groups, num_n, bm;       // bm = rows per cluster tile (128 * CG)
+  __device__ __forceinline__ int num_tiles() const { return tile_off[n_groups]; }
+  __device__ __forceinline__ TileCoord decode(int t) const {
+    int lo = 0, hi = n_groups - 1;  // last e with tile_off[e] <= t
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (tile_off[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int r = t - tile_off[e];
+    const int mtiles = (rows[e] + bm - 1) / bm;
+    TileCoord c;
+    c.e = e;
+    c.mt = r % mtiles;
+    c.nt = r / mtiles;
+    c.row_base = row_off[e];
+    c.rows = rows[e];
+    return c;
+  }
+  __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *, int e) const { return &y[e]; }
+};
+
+template <int CG, bool B_MN, typename OutT, typename Prob>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmC, int M, int N, int K, Sched sched) {
+                 const __grid_constant__ CUtensorMap tmC, int N, int K,
+                 const __grid_constant__ Prob sched) {
   using C = Cfg<CG, B_MN, OutT>;
+  constexpr bool GROUPED = Prob::kGrouped;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -92,7 +149,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const bool leader = (rank == 0);
   const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
   const int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
-  const int num_tiles = sched.num_m * sched.num_n;
+  const int num_tiles = sched.num_tiles();
   const int num_k = (K + BK - 1) / BK;
 
   if (warp == 0 && lane_id() == 0) {
@@ -122,10 +179,9 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       uint32_t phase = 0;
       const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), 0) : full_bar(0);
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        int mt, nt;
-        sched.tile(t, mt, nt);
-        const int m0 = mt * BM_CTA * CG + (int)rank * BM_CTA;
-        const int n0 = nt * BN + (int)rank * C::NB_CTA;
+        const TileCoord tc = sched.decode(t);
+        const int m0 = tc.row_base + tc.mt * BM_CTA * CG + (int)rank * BM_CTA;
+        const int n0 = tc.nt * BN + (int)rank * C::NB_CTA;
         for (int kb = 0; kb < num_k; ++kb) {
           if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
           else mbar_wait(empty_bar(stage), phase ^ 1, 1);
@@ -134,7 +190,21 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const uint32_t sa = sbase + stage * C::STAGE_BYTES;
           const uint32_t sb = sa + C::A_BYTES;
           const int k0 = kb * BK;
-          if constexpr (CG == 2) {
+          if constexpr (GROUPED) {
+            // W[e] through the 3-D map: (n, k, e) for [G,K,N], (k, n, e) for [G,N,K]
+            if constexpr (CG == 2) tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+            else tma_load_2d(sa, &tmA, fb, k0, m0);
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < C::NB_CTA / 64; ++j) {
+                if constexpr (CG == 2) tma_load_3d_cg2(sb + j * (64 * BK * 2), &tmB, fb, n0 + j * 64, k0, tc.e);
+                else tma_load_3d(sb + j * (64 * BK * 2), &tmB, fb, n0 + j * 64, k0, tc.e);
+              }
+            } else {
+              if constexpr (CG == 2) tma_load_3d_cg2(sb, &tmB, fb, k0, n0, tc.e);
+              else tma_load_3d(sb, &tmB, fb, k0, n0, tc.e);
+            }
+          } else if constexpr (CG == 2) {
             tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
             if constexpr (B_MN) {
 #pragma unroll
@@ -211,10 +281,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t acc_phase = 0;
     int buf = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      int mt, nt;
-      sched.tile(t, mt, nt);
-      const int row0 = mt * BM_CTA * CG + (int)rank * BM_CTA + q * 32;
-      const int col0 = nt * BN;
+      const TileCoord tc = sched.decode(t);
+      const int row0 = tc.mt * BM_CTA * CG + (int)rank * BM_CTA + q * 32;  // row in the C map
+      const int col0 = tc.nt * BN;
+      const CUtensorMap *cmap = sched.c_map(&tmC, tc.e);
       mbar_wait(tfull_bar(acc), acc_phase, 4);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -232,7 +302,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             else mbar_arrive(tempty_bar(acc));
           }
         }
-        const bool live = (row0 < M) && (col0 + ch * EPI_COLS < N);
+        const bool live = (row0 < tc.rows) && (col0 + ch * EPI_COLS < N);
         if (live) {
           // staging buffer `buf` was used two chunks ago: its store must have read smem
           if (lane == 0) bulk_wait_read<1>();
@@ -262,7 +332,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, sbuf, col0 + ch * EPI_COLS, row0);
+            tma_store_2d(cmap, sbuf, col0 + ch * EPI_COLS, row0);
             bulk_commit();
           }
           buf ^= 1;
@@ -282,30 +352,15 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
-template <int CG, bool B_MN, typename OutT>
-cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
+template <int CG, bool B_MN, typename OutT, typename Prob>
+cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CUtensorMap &tC, int n,
+                          int k, const Prob &prob, int tiles, int max_clusters, cudaStream_t stream) {
   using C = Cfg<CG, B_MN, OutT>;
-  const CUtensorMapDataType cdt =
-      sizeof(OutT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.k, g.lda, BK,
-                                BM_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
-  CUtensorMap tB = B_MN ? make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, g.ldb,
-                                       64, BK, CU_TENSOR_MAP_SWIZZLE_128B)
-                        : make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, g.ldb,
-                                       BK, C::NB_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
-  CUtensorMap tC = make_tmap_2d(g.c, cdt, sizeof(OutT), g.m, g.n, g.ldc, EPI_COLS, 32,
-                                sizeof(OutT) == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                  : CU_TENSOR_MAP_SWIZZLE_128B);
-  Sched s;
-  s.num_m = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
-  s.num_n = (int)((g.n + BN - 1) / BN);
-  s.group = g.raster_group > 0 ? g.raster_group : 8;
-  const int tiles = s.num_m * s.num_n;
   int clusters = sm_count() / CG;
-  if (g.max_clusters > 0 && g.max_clusters < clusters) clusters = g.max_clusters;
+  if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
   if (clusters > tiles) clusters = tiles;
-
-  auto kern = gemm_bf16_kernel<CG, B_MN, OutT>;
+  if (clusters <= 0) return cudaSuccess;
+  auto kern = gemm_bf16_kernel<CG, B_MN, OutT, Prob>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -320,7 +375,80 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, (int)g.m, (int)g.n, (int)g.k, s);
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, prob);
+}
+
+template <typename OutT>
+CUtensorMap make_c_map(const void *c, int64_t rows, int64_t n, int64_t ldc) {
+  const CUtensorMapDataType cdt =
+      sizeof(OutT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return make_tmap_2d(c, cdt, sizeof(OutT), rows, n, ldc, EPI_COLS, 32,
+                      sizeof(OutT) == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int CG, bool B_MN, typename OutT>
+cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
+  using C = Cfg<CG, B_MN, OutT>;
+  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.k, g.lda, BK,
+                                BM_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tB = B_MN ? make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, g.ldb,
+                                       64, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                        : make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, g.ldb,
+                                       BK, C::NB_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tC = make_c_map<OutT>(g.c, g.m, g.n, g.ldc);
+  Sched s;
+  s.num_m = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
+  s.num_n = (int)((g.n + BN - 1) / BN);
+  s.group = g.raster_group > 0 ? g.raster_group : 8;
+  s.M = (int)g.m;
+  return launch_kernel<CG, B_MN, OutT>(tA, tB, tC, (int)g.n, (int)g.k, s, s.num_m * s.num_n,
+                                       g.max_clusters, stream);
+}
+
+// One launch per chunk of <= MAX_GROUPS groups (the Y maps travel in the
+// kernel's parameter block).
+template <int CG, bool B_MN>
+cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
+  using C = Cfg<CG, B_MN, __nv_bfloat16>;
+  const int64_t total_rows = g.m_offsets[g.n_groups];
+  CUtensorMap tA = make_tmap_2d(g.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, total_rows, g.k, g.k, BK,
+                                BM_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  auto *gs = new GroupedSched;  // ~18 KB: keep it off the host stack
+  cudaError_t err = cudaSuccess;
+  for (int64_t g0 = 0; g0 < g.n_groups && err == cudaSuccess; g0 += MAX_GROUPS) {
+    const int cnt = (int)std::min<int64_t>(MAX_GROUPS, g.n_groups - g0);
+    const char *wbase = static_cast<const char *>(g.w) + (size_t)g0 * g.k * g.n * 2;
+    CUtensorMap tB = B_MN ? make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, cnt,
+                                         g.n, g.k * g.n, 64, BK, 1, CU_TENSOR_MAP_SWIZZLE_128B)
+                          : make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, cnt,
+                                         g.k, g.k * g.n, BK, C::NB_CTA, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    std::memset(gs, 0, sizeof(GroupedSched));
+    gs->n_groups = cnt;
+    gs->num_n = (int)((g.n + BN - 1) / BN);
+    gs->bm = BM_CTA * CG;
+    int tiles = 0;
+    int first_live = -1;
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t r0 = g.m_offsets[g0 + i], r1 = g.m_offsets[g0 + i + 1];
+      gs->tile_off[i] = tiles;
+      gs->row_off[i] = (int)r0;
+      gs->rows[i] = (int)(r1 - r0);
+      tiles += (int)((r1 - r0 + gs->bm - 1) / gs->bm) * gs->num_n;
+      if (r1 > r0) {
+        gs->y[i] = make_c_map<__nv_bfloat16>(static_cast<char *>(g.y) + (size_t)r0 * g.n * 2,
+                                             r1 - r0, g.n, g.n);
+        if (first_live < 0) first_live = i;
+      }
+    }
+    gs->tile_off[cnt] = tiles;
+    if (tiles == 0) continue;
+    for (int i = 0; i < cnt; ++i)
+      if (gs->rows[i] == 0) gs->y[i] = gs->y[first_live];  // never stored through
+    err = launch_kernel<CG, B_MN, __nv_bfloat16>(tA, tB, gs->y[first_live], (int)g.n, (int)g.k, *gs,
+                                                 tiles, g.max_clusters, stream);
+  }
+  delete gs;
+  return err;
 }
 
 }  // namespace
@@ -340,6 +468,18 @@ cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream) {
   if (g.c_f32) return cg2 ? launch_impl<2, false, float>(g, stream) : launch_impl<1, false, float>(g, stream);
   return cg2 ? launch_impl<2, false, __nv_bfloat16>(g, stream)
              : launch_impl<1, false, __nv_bfloat16>(g, stream);
+}
+
+cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stream) {
+  if (g.n_groups <= 0 || g.n == 0 || g.m_offsets[g.n_groups] == g.m_offsets[0]) return cudaSuccess;
+  if (g.k == 0) {
+    const int64_t r0 = g.m_offsets[0], r1 = g.m_offsets[g.n_groups];
+    return cudaMemsetAsync(static_cast<char *>(g.y) + (size_t)r0 * g.n * 2, 0,
+                           (size_t)(r1 - r0) * g.n * 2, stream);
+  }
+  if (g.cta_group == 1)
+    return g.w_kn ? grouped_impl<1, true>(g, stream) : grouped_impl<1, false>(g, stream);
+  return g.w_kn ? grouped_impl<2, true>(g, stream) : grouped_impl<2, false>(g, stream);
 }
 
 }  // namespace mimw

@@ -19,4 +19,21 @@ struct GemmArgs {
 
 cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream);
 
+// Grouped (MoE) GEMM: for e < n_groups,
+//   y[off_e : off_{e+1}, :] = x[off_e : off_{e+1}, :] . W_e
+// with off = m_offsets (HOST array of n_groups + 1 non-decreasing rows),
+// x bf16 [off_G, k], w bf16 [G, k, n] (w_kn) or [G, n, k], y bf16 [off_G, n].
+struct GroupedGemmArgs {
+  const void *x;
+  const int64_t *m_offsets;
+  const void *w;
+  void *y;
+  int64_t n_groups, n, k;
+  bool w_kn;
+  int cta_group;
+  int max_clusters;
+};
+
+cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stream);
+
 }  // namespace mimw

@@ -209,6 +209,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const void *tmap,
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_cg2(uint32_t dst, const void *tmap,
+                                                uint32_t bar_cluster, int32_t x, int32_t y,
+                                                int32_t z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
 // 2-SM form with multicast: the box is written at offset `dst` in every CTA
 // of `mask`; each destination's completion goes to the barrier at the same
 // offset in that CTA's pair leader.

@@ -70,3 +70,26 @@ def test_bad_enum_is_arg_error(L):
     r = L.mimw_b200_gemm_bf16(None, None, None, 4, 4, 4, 4, 4, 4, 7, 0, None)
     assert r == 4
     assert b"b_layout" in L.mimw_b200_last_error()
+
+
+def test_grouped_gemm_argument_errors(L):
+    """Shape / argument validation happens before any device work."""
+    import ctypes
+    offs = (ctypes.c_int64 * 3)(0, 5, 3)  # decreasing
+    r = L.mimw_b200_grouped_gemm_bf16(None, offs, None, None, 2, 64, 64, 0, None)
+    assert r == 1 and b"non-decreasing" in L.mimw_b200_last_error()
+    offs = (ctypes.c_int64 * 3)(0, 5, 9)
+    r = L.mimw_b200_grouped_gemm_bf16(None, offs, None, None, 2, 64, 64, 9, None)
+    assert r == 4
+    r = L.mimw_b200_grouped_gemm_bf16(None, None, None, None, 2, 64, 64, 0, None)
+    assert r == 4
+
+
+def test_oracle_grouped_gemm_is_per_group_oracle_gemm():
+    import oracle
+    offs = [0, 3, 3, 8]
+    x = oracle.random_tile([8, 16], 1)
+    w = oracle.random_tile([3, 16, 24], 2)
+    ys = oracle.oracle_grouped_gemm(x, offs, w)
+    assert ys[1].shape == (0, 24)
+    np.testing.assert_array_equal(ys[2], oracle.oracle_gemm(x[3:8], w[2]))

@@ -1,0 +1,126 @@
+"""GPU parity: grouped (MoE) bf16 GEMM (BASELINE.json configs[4]) vs the
+oracle — one oracle_gemm (oracles.cpp:14-26) per group.
+
+Tolerance: fp32 accumulate, bf16 output; the reference rel_error
+(case.cpp:94-104) per group <= 1e-2 (north_star bf16), and in fact within
+one bf16 rounding (<= 2^-8) of the oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2
+ROUND_TOL = 2.0 ** -8
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2605_10905_b200 as P
+    P.lib()
+    return P
+
+
+def _case(rows, k, n, seed, start=0, extra=0):
+    import torch
+    offs = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64) + start
+    total = int(offs[-1]) + extra
+    x = oracle.round_bf16(oracle.random_tile([total, k], oracle.input_seed(seed, 0)))
+    w = oracle.round_bf16(oracle.random_tile([len(rows), k, n], oracle.input_seed(seed, 1)))
+    tx = torch.from_numpy(x).cuda().bfloat16()
+    tw = torch.from_numpy(w).cuda().bfloat16()
+    return offs, x, w, tx, tw
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("w_layout", ["kn", "nk"])
+def test_grouped_ragged_full_oracle(P, cta_group, w_layout):
+    """Ragged groups incl. empty, 1-row, exact-tile and tail-tile experts;
+    K and N not multiples of the tile; rows outside every group untouched."""
+    import torch
+    rows = [0, 1, 130, 256, 0, 300, 77]
+    offs, x, w, tx, tw = _case(rows, 264, 328, 11, start=5, extra=9)
+    tww = tw if w_layout == "kn" else tw.transpose(1, 2).contiguous()
+    out = torch.full((x.shape[0], 328), 3.0, device="cuda", dtype=torch.bfloat16)
+    P.grouped_gemm(tx, offs, tww, out=out, w_layout=P.B_KN if w_layout == "kn" else P.B_NK,
+                   cta_group=cta_group)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    want = oracle.oracle_grouped_gemm(x, offs, w)
+    for e in range(len(rows)):
+        ge = got[offs[e]:offs[e + 1]]
+        if rows[e] == 0:
+            continue
+        assert oracle.rel_error(ge, want[e]) <= ROUND_TOL, e
+        assert oracle.rel_error_rows(ge, want[e]) <= BF16_TOL, e
+    # rows before the first and after the last group keep the sentinel
+    assert np.all(got[:offs[0]] == 3.0) and np.all(got[offs[-1]:] == 3.0)
+
+
+def test_grouped_more_than_128_groups(P):
+    """More groups than one launch's parameter block holds (chunked launches)."""
+    import torch
+    rng = np.random.default_rng(3)
+    rows = list(rng.integers(0, 40, size=150))
+    offs, x, w, tx, tw = _case(rows, 64, 64, 12)
+    got = P.grouped_gemm(tx, offs, tw).float().cpu().numpy()
+    want = oracle.oracle_grouped_gemm(x, offs, w)
+    for e in range(len(rows)):
+        if rows[e]:
+            assert oracle.rel_error(got[offs[e]:offs[e + 1]], want[e]) <= ROUND_TOL, e
+
+
+def test_grouped_all_empty_and_k_zero(P):
+    import torch
+    tw = torch.zeros((3, 0, 64), device="cuda", dtype=torch.bfloat16)
+    tx = torch.zeros((10, 0), device="cuda", dtype=torch.bfloat16)
+    out = torch.full((10, 64), 5.0, device="cuda", dtype=torch.bfloat16)
+    P.grouped_gemm(tx, [0, 4, 4, 10], tw, out=out)
+    assert torch.count_nonzero(out).item() == 0
+    tw = torch.ones((2, 64, 64), device="cuda", dtype=torch.bfloat16)
+    tx = torch.ones((4, 64), device="cuda", dtype=torch.bfloat16)
+    out = torch.full((4, 64), 5.0, device="cuda", dtype=torch.bfloat16)
+    P.grouped_gemm(tx, [0, 0, 0], tw, out=out)  # no rows: nothing written
+    assert torch.all(out == 5.0)
+
+
+def moe_counts(tokens=16384, top_k=2, experts=64, seed=5):
+    """configs[4] routing: Dirichlet(1) expert probabilities, multinomial
+    assignment of tokens*top_k rows."""
+    rng = np.random.default_rng(seed)
+    p = rng.dirichlet(np.ones(experts))
+    return rng.multinomial(tokens * top_k, p)
+
+
+def test_grouped_moe_config_sampled(P):
+    """configs[4] size (64 experts, K=4096, N=14336, ragged Dirichlet counts):
+    sampled rows of several experts against the exact oracle, plus a
+    per-expert column-sum (linearity) check over every row."""
+    import torch
+    counts = moe_counts()
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    K, N, G = 4096, 14336, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    tx = (torch.rand((int(offs[-1]), K), device="cuda", generator=g) * 2 - 1).bfloat16()
+    tw = (torch.rand((G, K, N), device="cuda", generator=g) * 2 - 1).bfloat16()
+    y = P.grouped_gemm(tx, offs, tw)
+    torch.cuda.synchronize()
+    order = np.argsort(counts)
+    for e in [int(order[0]), int(order[G // 2]), int(order[-1])]:
+        if counts[e] == 0:
+            continue
+        r = sorted({0, int(counts[e]) - 1, int(counts[e]) // 2})
+        xe = tx[offs[e]:offs[e + 1]][r].float().cpu().numpy()
+        want = oracle.oracle_gemm(xe, tw[e].float().cpu().numpy())
+        got = y[offs[e]:offs[e + 1]][r].float().cpu().numpy()
+        assert oracle.rel_error(got, want) <= BF16_TOL, e
+        # linearity over all rows of the expert
+        ones = torch.ones((1, int(counts[e])), device="cuda", dtype=torch.float64)
+        lhs = ones @ y[offs[e]:offs[e + 1]].double()
+        rhs = (ones @ tx[offs[e]:offs[e + 1]].double()) @ tw[e].double()
+        assert (torch.max(torch.abs(lhs - rhs)) / torch.max(torch.abs(rhs))).item() < 1e-2, e

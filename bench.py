@@ -155,6 +155,24 @@ def timed(step, steps, warmup, ws, stream):
     return max_over_ranks(e0.elapsed_time(e1) / 1e3, ws)
 
 
+def reassembly_ms(fn, ws, reps=5):
+    """Device time of one output reassembly (NCCL all-gather over NVLink),
+    max over ranks; reported next to the compute-only value."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / reps, ws)
+    return {"op": "ncclAllGather (torch.distributed all_gather_into_tensor)", "ms": round(ms, 4)}
+
+
 # ---------------------------------------------------------------------------
 # CPU reference path (oracle/_ref = the unmodified reference oracles)
 # ---------------------------------------------------------------------------
@@ -310,9 +328,10 @@ def bench_attention(args, rank, ws, local):
     L = P.lib()
     pk = peaks()
     dev = torch.device("cuda", local)
+    from paper_2605_10905_b200 import shard
     bh = FA_B * FA_H
-    assert bh % ws == 0
-    my = bh // ws
+    ranges = shard.head_shards(bh, ws)
+    my = ranges[rank][1] - ranges[rank][0]
     g = torch.Generator(device=dev).manual_seed(31 + rank)
     q, k, v = ((torch.rand((my, 1, FA_S, FA_D), device=dev, generator=g) * 2 - 1)
                .to(torch.bfloat16) for _ in range(3))
@@ -336,9 +355,15 @@ def bench_attention(args, rank, ws, local):
     flop_mine = flop_total / ws
     value = flop_total * steps / secs / 1e12
     achieved = flop_mine / (secs / steps) / 1e12
+    reasm = None
+    if ws > 1:  # NCCL all-gather of O and LSE, reported beside (not inside) the compute number
+        reasm = reassembly_ms(lambda: (shard.all_gather_rows(o, ranges),
+                                       shard.all_gather_rows(lse, ranges)), ws)
+        reasm["bytes_gathered"] = bh * FA_S * (FA_D * 2 + 4)
     res = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws,
            "steps": steps, "warmup": args.warmup, "ms_per_step": round(secs / steps * 1e3, 4),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+           "reassembly": reasm,
            "data": "synthetic U[-1,1] bf16",
            "config": {"workload": "configs[3]: causal flash-attention forward bf16 B=4 H=32 "
                                   "S=8192 D=128, batch x head sharded",
@@ -426,13 +451,15 @@ def bench_moe(args, rank, ws, local):
     L = P.lib()
     pk = peaks()
     dev = torch.device("cuda", local)
+    from paper_2605_10905_b200 import shard
     counts = moe_counts()
-    assert MOE_E % ws == 0
-    per = MOE_E // ws
-    mine = counts[rank * per:(rank + 1) * per]
+    parts = shard.expert_shards(counts, ws)
+    e0, e1 = parts[rank]
+    per = e1 - e0
+    mine = counts[e0:e1]
     offs = np.concatenate([[0], np.cumsum(mine)]).astype(np.int64)
     g = torch.Generator(device=dev).manual_seed(5 + rank)
-    w = torch.empty((per, MOE_K, MOE_N), device=dev, dtype=torch.bfloat16)
+    w = torch.empty((max(1, per), MOE_K, MOE_N), device=dev, dtype=torch.bfloat16)
     for e in range(per):  # chunked init keeps the fp32 temporaries small
         w[e] = (torch.rand((MOE_K, MOE_N), device=dev, generator=g) * 2 - 1).bfloat16()
     x = (torch.rand((max(1, int(offs[-1])), MOE_K), device=dev, generator=g) * 2 - 1).bfloat16()
@@ -456,7 +483,14 @@ def bench_moe(args, rank, ws, local):
     per_launch = secs / steps
     achieved = flop_mine / per_launch / 1e12
     bytes_mine = 2.0 * (per * MOE_K * MOE_N + int(offs[-1]) * (MOE_K + MOE_N))
-    return {"metric": METRIC, "value": round(flop_total * steps / secs / 1e12, 2), "unit": "TFLOPS",
+    reasm = None
+    if ws > 1:
+        full_offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        row_ranges = [shard.group_rows(full_offs, r) for r in parts]
+        yl = y[:int(offs[-1])]
+        reasm = reassembly_ms(lambda: shard.all_gather_rows(yl, row_ranges), ws)
+        reasm["bytes_gathered"] = int(counts.sum()) * MOE_N * 2
+    return {"reassembly": reasm, "metric": METRIC, "value": round(flop_total * steps / secs / 1e12, 2), "unit": "TFLOPS",
             "n_gpus": ws, "steps": steps, "warmup": args.warmup,
             "ms_per_step": round(per_launch * 1e3, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -465,7 +499,8 @@ def bench_moe(args, rank, ws, local):
                                    "ragged token counts, sharded by expert",
                        "experts": MOE_E, "K": MOE_K, "N": MOE_N,
                        "rows": rows_total, "rows_min_max": [int(counts.min()), int(counts.max())],
-                       "parallelism": f"{per} of {MOE_E} experts per GPU",
+                       "parallelism": f"experts [{e0},{e1}) of {MOE_E} on rank {rank} "
+                                      "(contiguous min-max tile partition)",
                        "l2": "weights 7.5 GB > 126 MB L2 (no flush)"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
                          "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
@@ -534,12 +569,14 @@ def main():
         if not args.no_secondary:
             fa = bench_attention(args, rank, ws, local)
             res["secondary"] = {"attention_fwd": {k: fa[k] for k in (
-                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks")}}
+                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks",
+                "reassembly")}}
             res["secondary"]["mxfp8_gemm"] = bench_mxfp8(args, rank, ws, local)
             torch_empty_cache()
             moe = bench_moe(args, rank, ws, local)
             res["secondary"]["grouped_moe_gemm"] = {k: moe[k] for k in (
-                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks")}
+                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks",
+                "reassembly")}
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

@@ -52,6 +52,17 @@ def peaks():
     return dict(bf16=1590.0, bf16_sustained=1400.0, hbm=6650.0, src="fallback")
 
 
+def traffic(key):
+    """DRAM bytes per launch of the kernel from the committed ncu capture
+    (profiles/traffic.json, written from `ncu --set full` via tools/profile.sh)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[key]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (B200_PROFILING.md "clocks DURING the timed region")
 # ---------------------------------------------------------------------------
@@ -311,7 +322,8 @@ def bench_gemm(args, rank, ws, local):
                      "peak": pk["bf16"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
                      "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
                      "frac_of_spec_2250": round(achieved / 2250.0, 4),
-                     "traffic": None,
+                     "traffic": traffic("gemm_bf16_8192"),
+                     "algorithmic_bytes_min": 2.0 * (GEMM_M * GEMM_K + GEMM_K * GEMM_N + GEMM_M * GEMM_N),
                      "algorithmic_flop_per_launch": flop},
         "e2e": e2e,
         "gpu_launches": args.steps,
@@ -374,7 +386,8 @@ def bench_attention(args, rank, ws, local):
                         "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
                         "frac_of_spec_2250": round(achieved / 2250.0, 4),
                         "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
-                        "traffic": None, "algorithmic_flop_per_launch": flop_mine},
+                        "traffic": traffic("attention_fwd_b4h32s8192") if ws == 1 else None,
+                        "algorithmic_flop_per_launch": flop_mine},
            "gpu_launches": steps, "clocks": clocks}
     return res
 
@@ -427,7 +440,8 @@ def bench_mxfp8(args, rank, ws, local):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": 4500.0,
                          "unit": "TFLOP/s", "frac": round(achieved / 4500.0, 4),
                          "peak_source": "spec dense FP8 (no measured FP8 peak in MEASURED_PEAKS.json)",
-                         "cublas_fp8_scaled_mm_tflops_same_box": ref, "traffic": None},
+                         "cublas_fp8_scaled_mm_tflops_same_box": ref,
+                         "traffic": traffic("mxfp8_8192")},
             "clocks": clocks}
 
 
@@ -506,7 +520,8 @@ def bench_moe(args, rank, ws, local):
                          "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
                          "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
                          "hbm_gbs_min_bytes": round(bytes_mine / per_launch / 1e9, 1),
-                         "hbm_peak_gbs": pk["hbm"], "traffic": None,
+                         "hbm_peak_gbs": pk["hbm"],
+                         "traffic": traffic("grouped_moe") if ws == 1 else None,
                          "algorithmic_flop_per_launch": flop_mine},
             "gpu_launches": steps, "clocks": clocks}
 

@@ -1,0 +1,36 @@
+#!/bin/bash
+# ncu evidence for the hot-path kernels (run under gpurun, 1 GPU):
+#   launches.csv         every launch of a short default bench with its device time
+#                        (cold-cache, serialised: compare SHARES, not absolutes)
+#   <name>.ncu-rep       one `--set full` capture of each top kernel
+# Usage: tools/profile.sh [launches] [gemm] [fa] [fp8] [moe]
+set -u
+OUT=${OUT:-gpurun_out}
+mkdir -p "$OUT"
+NCU="ncu --clock-control none"
+for what in "$@"; do
+  case $what in
+    launches)
+      timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+        --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu \
+        > "$OUT/launches_bench.log" 2>&1 ;;
+    gemm)
+      timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
+        -k regex:"gemm_bf16_kernel.*::Sched>" -s 3 -c 1 -o "$OUT/gemm" -f \
+        python bench.py --workload gemm --no-secondary --steps 2 --warmup 3 --no-e2e --no-cpu \
+        > "$OUT/gemm_ncu.log" 2>&1 ;;
+    fa)
+      timeout 900 $NCU --set full --import-source on -k regex:attention_fwd_kernel -s 3 -c 1 \
+        -o "$OUT/fa" -f python bench.py --workload attention --steps 1 --warmup 3 --no-cpu \
+        > "$OUT/fa_ncu.log" 2>&1 ;;
+    fp8)
+      timeout 900 $NCU --set full --import-source on -k regex:mxfp8_kernel -s 3 -c 1 \
+        -o "$OUT/fp8" -f python bench.py --workload fp8 --steps 1 --warmup 3 --no-cpu \
+        > "$OUT/fp8_ncu.log" 2>&1 ;;
+    moe)
+      timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
+        -k regex:GroupedSched -s 3 -c 1 -o "$OUT/moe" -f \
+        python bench.py --workload moe --steps 1 --warmup 3 --no-cpu > "$OUT/moe_ncu.log" 2>&1 ;;
+  esac
+  echo "$what rc=$?"
+done

@@ -436,7 +436,8 @@ def bench_mxfp8(args, rank, ws, local):
     return {"value": round(ws * flop * steps / secs / 1e12, 2), "unit": "TFLOPS",
             "ms_per_step": round(secs / steps * 1e3, 4), "scaling": "weak",
             "config": {"workload": "configs[2]: MXFP8 e4m3 block-scaled GEMM M=N=K=8192 "
-                                   "(UE8M0 per 1x32 along K), bf16 out, 128x224x128 tiles"},
+                                   "(UE8M0 per 1x32 along K), bf16 out, 2-CTA 256x224x128 tiles (cta_group::2); "
+                                   "step includes the scale-factor atom reorder pre-pass"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": 4500.0,
                          "unit": "TFLOP/s", "frac": round(achieved / 4500.0, 4),
                          "peak_source": "spec dense FP8 (no measured FP8 peak in MEASURED_PEAKS.json)",

@@ -74,6 +74,7 @@ def _optional_sigs():
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
                                                                            C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
+        "mimw_b200_gemm_mxfp8_ex": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16_ex": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32,
                                            C.c_int32, C.c_int32, _vp],
@@ -206,7 +207,7 @@ def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None
     return out, lse
 
 
-def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None):
+def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None, cta_group: int = 2):
     """Block-scaled FP8 GEMM: a e4m3 [M,K], sfa uint8 (UE8M0) [M,K/32],
     b e4m3 [N,K], sfb [N,K/32]  ->  bf16 [M,N] = (a*2^(sfa-127)) . (b*2^(sfb-127))^T."""
     import torch
@@ -214,8 +215,8 @@ def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None):
     n = b.shape[0]
     if out is None:
         out = torch.empty((m, n), device=a.device, dtype=torch.bfloat16)
-    _check(lib().mimw_b200_gemm_mxfp8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), sfb.data_ptr(),
-                                      out.data_ptr(), m, n, k, _stream(stream)))
+    _check(lib().mimw_b200_gemm_mxfp8_ex(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), sfb.data_ptr(),
+                                         out.data_ptr(), m, n, k, cta_group, _stream(stream)))
     return out
 
 

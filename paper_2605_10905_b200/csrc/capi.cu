@@ -345,9 +345,9 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
   });
 }
 
-int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
-                         int64_t m, int64_t n, int64_t k, void *stream) {
-  return guarded([&] {
+static void gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
+                       int64_t m, int64_t n, int64_t k, int cta_group, void *stream) {
+  {
     require(m >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
     require(k % 32 == 0, MIMW_ERR_SHAPE, "k must be a multiple of the 32-element scale block");
     require(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
@@ -378,7 +378,22 @@ int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const vo
     g.ldb = k;
     g.ldc = n;
     g.workspace = ws.p;
+    g.cta_group = cta_group;
     check_cuda(mimw::gemm_mxfp8_launch(g, s), "mxfp8 gemm launch");
+  }
+}
+
+int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
+                         int64_t m, int64_t n, int64_t k, void *stream) {
+  return guarded([&] { gemm_mxfp8(a, sfa, b, sfb, c, m, n, k, 2, stream); });
+}
+
+// Test hook (not part of the public header): MXFP8 GEMM with forced cta_group.
+int mimw_b200_gemm_mxfp8_ex(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
+                            int64_t m, int64_t n, int64_t k, int32_t cta_group, void *stream) {
+  return guarded([&] {
+    require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
+    gemm_mxfp8(a, sfa, b, sfb, c, m, n, k, cta_group, stream);
   });
 }
 

@@ -5,13 +5,13 @@
 // The reference has no FP8; the oracle for this path is
 // oracle_gemm (proj/core/src/oracles.cpp:14-26) on the dequantised f32 Tiles
 // (oracle/oracle.c orc_mx_dequant).  Same MIMW roles as gemm_bf16.cu:
-//   warp 0      TMA producer: A/B tiles (cp.async.bulk.tensor, 128-B swizzle)
-//               and the stage's scale-factor atoms (cp.async.bulk), one
-//               mbarrier per stage with the total byte count
-//   warp 1      TMEM allocator + MMA issuer: tcgen05.cp moves the stage's
-//               scale factors smem -> TMEM (32x128b.warpx4), then 4 x
-//               tcgen05.mma.kind::mxf8f6f4.block_scale (K = 32 each, sf_id
-//               selects the k-block byte), commit frees the smem slot
+//   warp 0      TMA producer: A/B tiles and the stage's scale-factor atoms
+//               (all cp.async.bulk.tensor, 128-B swizzle for A/B), completing
+//               on the pair leader's `full[s]` with the stage's byte count
+//   warp 1      TMEM allocator + MMA issuer (pair leader): tcgen05.cp moves the
+//               stage's scale factors smem -> TMEM (32x128b.warpx4), then
+//               4 x tcgen05.mma.kind::mxf8f6f4.block_scale (K = 32 each, sf_id
+//               selects the k-block byte); the commit frees both CTAs' slots
 //   warps 2..5  epilogue: TMEM -> bf16 -> swizzled smem -> TMA store
 // Scale factors in TMEM (found with tools/sf_probe.cu): row m of A reads lane
 // m, column (m >> 5), byte sf_id; column n of B reads lane (n & 31), column
@@ -20,8 +20,13 @@
 // pre-pass (sf_tile_kernel) reorders the natural [rows, K/32] scale arrays
 // into per-tile atoms.
 //
-// Tile 128 x 224 x 128 (cta_group::1): two fp32 accumulators (2 x 224
-// columns) + double-buffered scale factors fit the 512 TMEM columns.
+// CG = 2 (default): a CTA pair runs M=256 x N=224 cta_group::2 MMAs.  Each
+// CTA stages its own 128 A rows and 112 of the 224 B rows (halving the
+// L2->smem traffic and the smem write bandwidth of the 1-CTA tile, the limit
+// of the FP8 rate), its own rows' SFA atom and the FULL tile's SFB atoms
+// (every CTA's D rows see all N columns).  The leader's tcgen05.cp.cta_group::2
+// copies each CTA's smem into that CTA's TMEM.  Two fp32 accumulators
+// (2 x 224 columns) + double-buffered scale factors fill the 512 TMEM columns.
 #include "gemm_mxfp8.h"
 #include "ptx.cuh"
 #include "tma_host.h"
@@ -32,34 +37,40 @@ namespace mimw {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 224;          // 7 x 32 columns
+constexpr int BM_CTA = 128;      // A rows per CTA
+constexpr int BN = 224;          // N per MMA / cluster tile (7 x 32 columns)
 constexpr int BK = 128;          // fp8 bytes per 128-B swizzle row = 4 scale blocks
 constexpr int UMMA_K = 32;
-constexpr int STAGES = 4;
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int EPI_COLS = 32;
-constexpr int A_BYTES = BM * BK;                 // 16 KiB
-constexpr int B_BYTES = BN * BK;                 // 28 KiB
 constexpr int SFA_BYTES = 512;                   // one atom: 128 rows x 4 k-blocks
 constexpr int SFB_BYTES = 1024;                  // two atoms: 256 (>= 224) columns
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 44 KiB, 1024-B aligned
-constexpr int SF_STAGE = SFA_BYTES + SFB_BYTES;  // scale-factor atoms of one stage
-constexpr int SF_OFF = STAGES * STAGE_BYTES;
+constexpr int SF_STAGE = SFA_BYTES + SFB_BYTES;
 constexpr int EPI_BUF = 32 * EPI_COLS * 2;       // bf16
 constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF;
-constexpr int EPI_OFF = SF_OFF + STAGES * SF_STAGE;
-constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
-constexpr int SMEM = BAR_OFF + 256 + 1024;
 constexpr uint32_t TM_ACC = 0;                   // 2 x 224 columns
 constexpr uint32_t TM_SF = 448;                  // per SF buffer: SFA 4 cols + SFB 8 cols
 constexpr uint32_t SF_STRIDE = 16;
 
-static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-B aligned for SWIZZLE_128B");
+template <int CG>
+struct Cfg {
+  static constexpr int NB_CTA = BN / CG;                        // B rows staged per CTA
+  static constexpr int A_BYTES = BM_CTA * BK;                   // 16 KiB
+  static constexpr int B_BYTES = NB_CTA * BK;                   // 14 / 28 KiB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int SF_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = SF_OFF + STAGES * SF_STAGE;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int TX = CG * (STAGE_BYTES + SF_STAGE);      // bytes landing per stage (pair)
+  static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-B aligned for SWIZZLE_128B");
+  static_assert(SMEM <= 232448, "smem budget");
+};
 
 struct Sched {
-  int num_m, num_n, group, kg;  // kg = K / 128 (scale-factor atoms per tile row)
+  int num_m, num_n, group;  // num_m in cluster tiles (128 * CG rows)
   __device__ __forceinline__ void tile(int t, int &mt, int &nt) const {
     int per_group = group * num_n;
     int g = t / per_group;
@@ -71,22 +82,30 @@ struct Sched {
   }
 };
 
+// tmSFA / tmSFB: the atom workspace viewed as [atoms * 2, 256] bytes
+// (TMA boxes of 256 x 2 = one SFA atom, 256 x 4 = the two SFB atoms of a tile).
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const __grid_constant__ CUtensorMap tmC, const uint8_t *__restrict__ sfa_t,
-                  const uint8_t *__restrict__ sfb_t, int M, int N, int K, Sched sched) {
+                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmSFA,
+                  const __grid_constant__ CUtensorMap tmSFB, int M, int N, int K, int KG, Sched sched) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_base = sbase + BAR_OFF;
+  const uint32_t bar_base = sbase + C::BAR_OFF;
   auto full_bar = [&](int s) { return bar_base + 8 * s; };
-  auto empty_bar = [&](int s) { return bar_base + 8 * (STAGES + s); };
-  auto tfull_bar = [&](int a) { return bar_base + 8 * (2 * STAGES + a); };
-  auto tempty_bar = [&](int a) { return bar_base + 8 * (2 * STAGES + 2 + a); };
-  const uint32_t tmem_slot = bar_base + 8 * (2 * STAGES + 4);
-  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 8 * (2 * STAGES + 4));
+  auto empty_bar = [&](int s) { return bar_base + 8 * (C::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + 2 + a); };
+  const uint32_t tmem_slot = bar_base + 8 * (2 * C::STAGES + 4);
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * C::STAGES + 4));
 
   const int warp = threadIdx.x / 32;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = (rank == 0);
+  const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
   const int num_tiles = sched.num_m * sched.num_n;
   const int num_k = (K + BK - 1) / BK;
 
@@ -94,19 +113,21 @@ gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
-    for (int s = 0; s < STAGES; ++s) {
+    tma_prefetch_desc(&tmSFA);
+    tma_prefetch_desc(&tmSFB);
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), EPI_WARPS);
+      mbar_init(tempty_bar(a), EPI_WARPS * CG);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
+  if (warp == 1) tmem_alloc<CG>(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
 
@@ -115,78 +136,99 @@ gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const uint32_t full0 = (CG == 2) ? map_to_rank(full_bar(0), 0) : full_bar(0);
+      for (int t = cluster; t < num_tiles; t += nclusters) {
         int mt, nt;
         sched.tile(t, mt, nt);
+        const int m128 = mt * CG + (int)rank;   // this CTA's 128-row block
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(empty_bar(stage), phase ^ 1, 1);
-          mbar_arrive_expect_tx(full_bar(stage), STAGE_BYTES + SF_STAGE);
-          const uint32_t sa = sbase + stage * STAGE_BYTES;
-          const uint32_t sb = sa + A_BYTES;
-          const uint32_t ssf = sbase + SF_OFF + stage * SF_STAGE;
-          tma_load_2d(sa, &tmA, full_bar(stage), kb * BK, mt * BM);
-          tma_load_2d(sb, &tmB, full_bar(stage), kb * BK, nt * BN);
-          bulk_load(ssf, sfa_t + ((size_t)mt * sched.kg + kb) * SFA_BYTES, SFA_BYTES, full_bar(stage));
-          bulk_load(ssf + SFA_BYTES, sfb_t + ((size_t)nt * sched.kg + kb) * SFB_BYTES, SFB_BYTES,
-                    full_bar(stage));
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
+          else mbar_wait(empty_bar(stage), phase ^ 1, 1);
+          const uint32_t fb = full0 + 8 * stage;
+          if (leader) mbar_arrive_expect_tx(full_bar(stage), C::TX);
+          const uint32_t sa = sbase + stage * C::STAGE_BYTES;
+          const uint32_t sb = sa + C::A_BYTES;
+          const uint32_t ssf = sbase + C::SF_OFF + stage * SF_STAGE;
+          const int sfa_row = (m128 * KG + kb) * 2;
+          const int sfb_row = (nt * KG + kb) * 4;
+          if constexpr (CG == 2) {
+            tma_load_2d_cg2(sa, &tmA, fb, kb * BK, m128 * BM_CTA);
+            tma_load_2d_cg2(sb, &tmB, fb, kb * BK, nt * BN + (int)rank * C::NB_CTA);
+            tma_load_2d_cg2(ssf, &tmSFA, fb, 0, sfa_row);
+            tma_load_2d_cg2(ssf + SFA_BYTES, &tmSFB, fb, 0, sfb_row);
+          } else {
+            tma_load_2d(sa, &tmA, fb, kb * BK, m128 * BM_CTA);
+            tma_load_2d(sb, &tmB, fb, kb * BK, nt * BN);
+            tma_load_2d(ssf, &tmSFA, fb, 0, sfa_row);
+            tma_load_2d(ssf + SFA_BYTES, &tmSFB, fb, 0, sfb_row);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    uint32_t sf_buf = 0;  // TMEM scale-factor double buffer (runs across tiles)
-    constexpr uint32_t HI_SW128 = (1024u >> 4) | (1u << 14) | (2u << 29);
-    constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      mbar_wait(tempty_bar(acc), acc_phase ^ 1, 2);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + TM_ACC + acc * BN;
-      for (int kb = 0; kb < num_k; ++kb) {
-        mbar_wait(full_bar(stage), phase, 3);
+    // ---------------- MMA issuer (pair leader) ----------------
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      uint32_t sf_buf = 0;  // TMEM scale-factor double buffer (runs across tiles)
+      constexpr uint32_t HI_SW128 = (1024u >> 4) | (1u << 14) | (2u << 29);
+      constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1, 2);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sa = sbase + stage * STAGE_BYTES;
-          const uint32_t sb = sa + A_BYTES;
-          const uint32_t ssf = sbase + SF_OFF + stage * SF_STAGE;
-          const uint32_t tsf = tmem_base + TM_SF + sf_buf * SF_STRIDE;
-          // scale factors smem -> TMEM (ordered before the MMAs in the tensor pipe)
-          tmem_cp_32x128b_warpx4(tsf, smem_desc_noswz(ssf, 128, 128));
-          tmem_cp_32x128b_warpx4(tsf + 4, smem_desc_noswz(ssf + SFA_BYTES, 128, 128));
-          tmem_cp_32x128b_warpx4(tsf + 8, smem_desc_noswz(ssf + SFA_BYTES + 512, 128, 128));
+        const uint32_t d_tmem = tmem_base + TM_ACC + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(full_bar(stage), phase, 3);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = sbase + stage * C::STAGE_BYTES;
+            const uint32_t sb = sa + C::A_BYTES;
+            const uint32_t ssf = sbase + C::SF_OFF + stage * SF_STAGE;
+            const uint32_t tsf = tmem_base + TM_SF + sf_buf * SF_STRIDE;
+            // scale factors smem -> TMEM (ordered before the MMAs in the tensor pipe)
+            tmem_cp_32x128b_warpx4<CG>(tsf, smem_desc_noswz(ssf, 128, 128));
+            tmem_cp_32x128b_warpx4<CG>(tsf + 4, smem_desc_noswz(ssf + SFA_BYTES, 128, 128));
+            tmem_cp_32x128b_warpx4<CG>(tsf + 8, smem_desc_noswz(ssf + SFA_BYTES + 512, 128, 128));
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            uint64_t ad, bd;
-            asm volatile("mov.b64 %0, {%1, %2};" : "=l"(ad) : "r"(LO_KMAJ | ((sa + k * 32) >> 4)), "r"(HI_SW128));
-            asm volatile("mov.b64 %0, {%1, %2};" : "=l"(bd) : "r"(LO_KMAJ | ((sb + k * 32) >> 4)), "r"(HI_SW128));
-            mma_mxf8_ss<1>(d_tmem, ad, bd, idesc_mxf8(BM, BN, k, k), tsf, tsf + 4, (kb | k) != 0);
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              uint64_t ad, bd;
+              asm volatile("mov.b64 %0, {%1, %2};" : "=l"(ad) : "r"(LO_KMAJ | ((sa + k * 32) >> 4)), "r"(HI_SW128));
+              asm volatile("mov.b64 %0, {%1, %2};" : "=l"(bd) : "r"(LO_KMAJ | ((sb + k * 32) >> 4)), "r"(HI_SW128));
+              mma_mxf8_ss<CG>(d_tmem, ad, bd, idesc_mxf8(BM_CTA * CG, BN, k, k), tsf, tsf + 4,
+                              (kb | k) != 0);
+            }
+            if constexpr (CG == 2) {
+              mma_commit_cg2_mc(empty_bar(stage), 0x3);
+              if (kb == num_k - 1) mma_commit_cg2_mc(tfull_bar(acc), 0x3);
+            } else {
+              mma_commit(empty_bar(stage));
+              if (kb == num_k - 1) mma_commit(tfull_bar(acc));
+            }
           }
-          mma_commit(empty_bar(stage));
-          if (kb == num_k - 1) mma_commit(tfull_bar(acc));
+          __syncwarp();
+          sf_buf ^= 1;
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        sf_buf ^= 1;
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     const int ew = warp - 2;
     const uint32_t lane = lane_id();
-    const uint32_t stage_base = sbase + EPI_OFF + ew * 2 * EPI_BUF;
+    const uint32_t stage_base = sbase + C::EPI_OFF + ew * 2 * EPI_BUF;
+    const uint32_t tempty_leader0 = (CG == 2) ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
     int acc = 0;
     uint32_t acc_phase = 0;
     int buf = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cluster; t < num_tiles; t += nclusters) {
       int mt, nt;
       sched.tile(t, mt, nt);
-      const int row0 = mt * BM + q * 32;
+      const int row0 = (mt * CG + (int)rank) * BM_CTA + q * 32;
       const int col0 = nt * BN;
       mbar_wait(tfull_bar(acc), acc_phase, 4);
       tc_fence_after();
@@ -199,7 +241,10 @@ gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         if (ch == BN / EPI_COLS - 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(tempty_bar(acc));
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + 8 * acc);
+            else mbar_arrive(tempty_bar(acc));
+          }
         }
         if (row0 < M && col0 + ch * EPI_COLS < N) {
           if (lane == 0) bulk_wait_read<1>();
@@ -231,77 +276,109 @@ gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem_base, 512);
+    tmem_dealloc<CG>(tmem_base, 512);
   }
 }
 
 // Reorder natural [rows, kb] UE8M0 scales into per-tile atoms:
-//   atom(tile, kg, half)[r*16 + c*4 + y] = sf[tile*rows_per_tile + half*128 + 32c + r, 4kg + y]
-// (127 = 1.0 outside the matrix).  One thread per output byte.
-__global__ void sf_tile_kernel(const uint8_t *__restrict__ sf, int rows, int kb, int rows_per_tile,
-                               int halves, int tiles, int kg, uint8_t *__restrict__ out) {
-  const int64_t total = (int64_t)tiles * kg * halves * 512;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int byte = (int)(i & 511);
-    int64_t atom = i >> 9;
-    const int half = (int)(atom % halves);
-    atom /= halves;
-    const int g = (int)(atom % kg);
-    const int tile = (int)(atom / kg);
-    const int r = byte >> 4, c = (byte >> 2) & 3, y = byte & 3;
-    const int local = half * 128 + 32 * c + r;
-    const int row = tile * rows_per_tile + local;
-    const int k = 4 * g + y;
-    uint8_t v = 127;
-    if (local < rows_per_tile && row < rows && k < kb) v = sf[(size_t)row * kb + k];
-    out[i] = v;
+//   atom(tile, g, half)[r*16 + c*4 + y] = sf[tile*rows_per_tile + half*128 + 32c + r, 4g + y]
+// (127 = 1.0 outside the matrix).  One CTA per (tile, half, 8 k-groups); each warp writes
+// whole 512-byte atoms, one 16-byte line (lane r: rows 32c + r, c = 0..3) per
+// thread, so the stores are coalesced and every input sector is consumed by
+// the CTA (the 8 warps walk 8 consecutive k-groups = 32 bytes of each row).
+__global__ void __launch_bounds__(256) sf_tile_kernel(const uint8_t *__restrict__ sf, int rows, int kb,
+                                                      int rows_per_tile, int halves, int kg,
+                                                      uint8_t *__restrict__ out) {
+  const int tile = blockIdx.x, half = blockIdx.y;
+  const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int local0 = half * 128 + r;
+  for (int g = blockIdx.z * 8 + w; g < kg; g += 8 * gridDim.z) {
+    uint32_t word[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int local = local0 + 32 * c;
+      const int row = tile * rows_per_tile + local;
+      uint32_t v = 0;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int k = 4 * g + y;
+        uint32_t b = 127;
+        if (local < rows_per_tile && row < rows && k < kb) b = __ldg(sf + (size_t)row * kb + k);
+        v |= b << (8 * y);
+      }
+      word[c] = v;
+    }
+    uint8_t *dst = out + ((size_t)((size_t)tile * kg + g) * halves + half) * 512 + r * 16;
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(word[0], word[1], word[2], word[3]);
   }
 }
 
 }  // namespace
 
+// Workspace: SFA atoms [ceil(m/128)][KG] x 512 B, then SFB atoms
+// [ceil(n/224)][KG][2] x 512 B (KG = ceil(k/128)).
 size_t gemm_mxfp8_workspace(int64_t m, int64_t n, int64_t k) {
   const int64_t kg = (k + BK - 1) / BK;
-  const int64_t mt = (m + BM - 1) / BM, nt = (n + BN - 1) / BN;
-  return (size_t)(mt * kg * SFA_BYTES + nt * kg * SFB_BYTES);
+  const int64_t m128 = (m + BM_CTA - 1) / BM_CTA + 1;  // +1: a pair's odd tail block
+  const int64_t nt = (n + BN - 1) / BN;
+  return (size_t)(m128 * kg * SFA_BYTES + nt * kg * SFB_BYTES);
 }
 
-cudaError_t gemm_mxfp8_launch(const Mxfp8Args &g, cudaStream_t stream) {
+template <int CG>
+cudaError_t launch_cg(const Mxfp8Args &g, cudaStream_t stream) {
+  using Cf = Cfg<CG>;
   const int kg = (int)((g.k + BK - 1) / BK);
-  const int num_m = (int)((g.m + BM - 1) / BM), num_n = (int)((g.n + BN - 1) / BN);
+  const int num_m = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
+  const int num_n = (int)((g.n + BN - 1) / BN);
+  const int m128 = num_m * CG;
   uint8_t *sfa_t = static_cast<uint8_t *>(g.workspace);
-  uint8_t *sfb_t = sfa_t + (size_t)num_m * kg * SFA_BYTES;
+  uint8_t *sfb_t = sfa_t + (size_t)m128 * kg * SFA_BYTES;
   const int kb = (int)(g.k / 32);
-  {
-    int64_t na = (int64_t)num_m * kg * 512, nb = (int64_t)num_n * kg * 2 * 512;
-    sf_tile_kernel<<<(int)std::min<int64_t>((na + 255) / 256, 4096), 256, 0, stream>>>(
-        static_cast<const uint8_t *>(g.sfa), (int)g.m, kb, BM, 1, num_m, kg, sfa_t);
-    sf_tile_kernel<<<(int)std::min<int64_t>((nb + 255) / 256, 4096), 256, 0, stream>>>(
-        static_cast<const uint8_t *>(g.sfb), (int)g.n, kb, BN, 2, num_n, kg, sfb_t);
-  }
-  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.m, g.k, g.lda, BK, BM,
+  const int gz = (kg + 7) / 8;
+  sf_tile_kernel<<<dim3(m128, 1, gz), 256, 0, stream>>>(static_cast<const uint8_t *>(g.sfa), (int)g.m, kb,
+                                                    BM_CTA, 1, kg, sfa_t);
+  sf_tile_kernel<<<dim3(num_n, 2, gz), 256, 0, stream>>>(static_cast<const uint8_t *>(g.sfb), (int)g.n, kb,
+                                                     BN, 2, kg, sfb_t);
+  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.m, g.k, g.lda, BK, BM_CTA,
                                 CU_TENSOR_MAP_SWIZZLE_128B);
-  CUtensorMap tB = make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.n, g.k, g.ldb, BK, BN,
+  CUtensorMap tB = make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.n, g.k, g.ldb, BK, Cf::NB_CTA,
                                 CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tC = make_tmap_2d(g.c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.n, g.ldc, EPI_COLS,
                                 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap tSFA = make_tmap_2d(sfa_t, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)m128 * kg * 2,
+                                  256, 256, 256, 2, CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap tSFB = make_tmap_2d(sfb_t, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)num_n * kg * 4,
+                                  256, 256, 256, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
   Sched s;
   s.num_m = num_m;
   s.num_n = num_n;
-  s.group = 16;
-  s.kg = kg;
+  s.group = CG == 2 ? 8 : 16;
   const int tiles = num_m * num_n;
-  int grid = sm_count();
-  if (grid > tiles) grid = tiles;
-  cudaError_t e = cudaFuncSetAttribute(gemm_mxfp8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  int clusters = sm_count() / CG;
+  if (clusters > tiles) clusters = tiles;
+  auto kern = gemm_mxfp8_kernel<CG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
   if (e != cudaSuccess) return e;
-  gemm_mxfp8_kernel<<<grid, NUM_THREADS, SMEM, stream>>>(tA, tB, tC, sfa_t, sfb_t, (int)g.m, (int)g.n,
-                                                           (int)g.k, s);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tSFA, tSFB, (int)g.m, (int)g.n, (int)g.k, kg, s);
+}
+
+cudaError_t gemm_mxfp8_launch(const Mxfp8Args &g, cudaStream_t stream) {
+  return g.cta_group == 1 ? launch_cg<1>(g, stream) : launch_cg<2>(g, stream);
 }
 
 }  // namespace mimw

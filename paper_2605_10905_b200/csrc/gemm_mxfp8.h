@@ -14,6 +14,7 @@ struct Mxfp8Args {
   void *c;          // bf16 [m, n], row stride ldc
   int64_t m, n, k, lda, ldb, ldc;
   void *workspace;  // gemm_mxfp8_workspace(m, n, k) bytes (scale-factor atoms)
+  int cta_group;    // 2 (default, CTA pair M=256) or 1
 };
 
 size_t gemm_mxfp8_workspace(int64_t m, int64_t n, int64_t k);

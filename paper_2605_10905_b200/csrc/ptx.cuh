@@ -467,8 +467,14 @@ namespace mimw {
 
 // tcgen05.cp smem -> TMEM, 32 lanes x 128 bit, replicated to the 4 lane
 // quarters (the UE8M0 scale-factor staging used by the block-scaled MMA).
+// With CG = 2 the pair leader's instruction copies each CTA's smem (same
+// offset) into that CTA's TMEM (same address).
+template <int CG = 1>
 __device__ __forceinline__ void tmem_cp_32x128b_warpx4(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+  else
+    asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
 // No-swizzle (interleaved) shared-memory descriptor: 8-row x 16-byte core

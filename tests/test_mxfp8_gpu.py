@@ -31,14 +31,16 @@ def _mx_operand(rows, k, seed):
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 224, 128), (256, 448, 512), (300, 504, 1056), (1, 8, 32),
-                                   (1024, 1024, 1024)])
-def test_mxfp8_vs_dequant_oracle(P, m, n, k):
+                                   (1024, 1024, 1024), (520, 8192, 160)])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_mxfp8_vs_dequant_oracle(P, m, n, k, cta_group):
     import torch
     qa, sfa = _mx_operand(m, k, m + k)
     qb, sfb = _mx_operand(n, k, n + 3 * k)
     ta, tb = torch.from_numpy(qa).cuda(), torch.from_numpy(qb).cuda()
     tsa, tsb = torch.from_numpy(sfa).cuda(), torch.from_numpy(sfb).cuda()
-    c = P.gemm_mxfp8(ta.view(torch.float8_e4m3fn), tsa, tb.view(torch.float8_e4m3fn), tsb)
+    c = P.gemm_mxfp8(ta.view(torch.float8_e4m3fn), tsa, tb.view(torch.float8_e4m3fn), tsb,
+                     cta_group=cta_group)
     torch.cuda.synchronize()
     got = c.float().cpu().numpy()
     assert np.isfinite(got).all()

@@ -25,6 +25,7 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 DEBUG = ["-DMIMW_WATCHDOG_PRINTF"] if os.environ.get("MIMW_DEBUG") else []
+DEBUG += os.environ.get("MIMW_NVCC_EXTRA", "").split()  # e.g. -DMIMW_FA_TRACE (tools/fa_trace.py)
 FLAGS = DEBUG + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                 "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 

@@ -452,7 +452,8 @@ int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int
                            int32_t cta_group, int32_t raster_group, int32_t max_clusters,
                            void *stream) {
   return guarded([&] {
-    require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
+    require(cta_group == 1 || cta_group == 2 || cta_group == 4, MIMW_ERR_ARG,
+            "cta_group must be 1, 2 or 4 (two CTA pairs sharing B by multicast)");
     if (m == 0 || n == 0) return;
     if (k == 0) {  // C = 0 (oracles.cpp:19)
       require(c != nullptr, MIMW_ERR_ARG, "null pointer");
@@ -478,7 +479,8 @@ int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int
     g.ldc = ldc;
     g.b_kn = b_layout == MIMW_B_KN;
     g.c_f32 = c_dtype == MIMW_F32;
-    g.cta_group = cta_group;
+    g.cta_group = cta_group == 4 ? 2 : cta_group;
+    g.cluster_pairs = cta_group == 4 ? 2 : 1;
     g.raster_group = raster_group;
     g.max_clusters = max_clusters;
     check_cuda(mimw::gemm_bf16_launch(g, static_cast<cudaStream_t>(stream)), "gemm launch");

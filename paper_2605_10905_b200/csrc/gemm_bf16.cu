@@ -70,9 +70,11 @@ struct TileCoord {
 
 // Dense problem: one [M,K] x B -> [M,N]; grouped-rasterised tile order
 // (`group` M-tiles share each N sweep so B panels are re-read from L2).
-struct Sched {
+template <int PAIRS>
+struct SchedT {
   static constexpr bool kGrouped = false;
-  int num_m, num_n, group, M;
+  static constexpr int kPairs = PAIRS;  // CTA pairs per cluster sharing each B tile (multicast)
+  int num_m, num_n, group, M;           // num_m in cluster tiles (PAIRS M-tiles each)
   __device__ __forceinline__ int num_tiles() const { return num_m * num_n; }
   __device__ __forceinline__ TileCoord decode(int t) const {
     int per_group = group * num_n;
@@ -84,12 +86,14 @@ struct Sched {
     c.e = 0;
     c.mt = first_m + r % gsize;
     c.nt = r / gsize;
+    if (g & 1) c.nt = num_n - 1 - c.nt;  // boustrophedon: reuse the B panels still in L2
     c.row_base = 0;
     c.rows = M;
     return c;
   }
   __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *tmC, int) const { return tmC; }
 };
+using Sched = SchedT<1>;
 
 // Grouped (MoE) problem: Y_e[m_e, N] = X[row_off_e : row_off_e + m_e, K] . W_e
 // for e < n_groups.  X rows are packed by group; W is one [G, K, N] (or
@@ -100,6 +104,7 @@ struct Sched {
 constexpr int MAX_GROUPS = 128;
 struct GroupedSched {
   static constexpr bool kGrouped = true;
+  static constexpr int kPairs = 1;
   CUtensorMap y[MAX_GROUPS];
   int tile_off[MAX_GROUPS + 1];  // prefix sum of m_tiles(e) * num_n
   int row_off[MAX_GROUPS];       // first row of group e in X / Y
@@ -133,6 +138,11 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                  const __grid_constant__ Prob sched) {
   using C = Cfg<CG, B_MN, OutT>;
   constexpr bool GROUPED = Prob::kGrouped;
+  // PAIRS = 2: a cluster of two CTA pairs computes two vertically adjacent
+  // 256x256 tiles; each B half-tile is loaded once and multicast to the
+  // same-rank CTA of both pairs (half the L2->smem traffic for B).
+  constexpr int PAIRS = Prob::kPairs;
+  static_assert(PAIRS == 1 || CG == 2, "multicast pairs need cta_group::2");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -145,7 +155,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * C::STAGES + 2 * ACC_STAGES));
 
   const int warp = threadIdx.x / 32;
-  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0;
+  const uint32_t rank = crank & (CG - 1);   // rank inside the CTA pair
+  const int pair = (int)(crank >> 1);       // pair inside the cluster (PAIRS == 2)
+  const uint32_t my_leader = crank & ~1u;
   const bool leader = (rank == 0);
   const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
   const int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
@@ -158,7 +171,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), PAIRS);
     }
     for (int a = 0; a < ACC_STAGES; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -177,10 +190,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), 0) : full_bar(0);
+      const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), my_leader) : full_bar(0);
       for (int t = cluster; t < num_tiles; t += nclusters) {
         const TileCoord tc = sched.decode(t);
-        const int m0 = tc.row_base + tc.mt * BM_CTA * CG + (int)rank * BM_CTA;
+        const int m0 = tc.row_base + (tc.mt * PAIRS + pair) * BM_CTA * CG + (int)rank * BM_CTA;
         const int n0 = tc.nt * BN + (int)rank * C::NB_CTA;
         for (int kb = 0; kb < num_k; ++kb) {
           if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
@@ -203,6 +216,18 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             } else {
               if constexpr (CG == 2) tma_load_3d_cg2(sb, &tmB, fb, k0, n0, tc.e);
               else tma_load_3d(sb, &tmB, fb, k0, n0, tc.e);
+            }
+          } else if constexpr (PAIRS == 2) {
+            tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+            if (pair == (int)rank) {  // one issuer per B half, multicast to both pairs
+              const uint16_t mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+              if constexpr (B_MN) {
+#pragma unroll
+                for (int j = 0; j < C::NB_CTA / 64; ++j)
+                  tma_load_2d_cg2_mc(sb + j * (64 * BK * 2), &tmB, fb, n0 + j * 64, k0, mask);
+              } else {
+                tma_load_2d_cg2_mc(sb, &tmB, fb, k0, n0, mask);
+              }
             }
           } else if constexpr (CG == 2) {
             tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
@@ -257,8 +282,9 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               mma_f16_ss<CG>(d_tmem, a_k, b_k, C::IDESC, (kb | k) != 0);
             }
             if constexpr (CG == 2) {
-              mma_commit_cg2_mc(empty_bar(stage), 0x3);
-              if (kb == num_k - 1) mma_commit_cg2_mc(tfull_bar(acc), 0x3);
+              // a stage is free once every pair that received its B has consumed it
+              mma_commit_cg2_mc(empty_bar(stage), PAIRS == 2 ? 0xF : 0x3);
+              if (kb == num_k - 1) mma_commit_cg2_mc(tfull_bar(acc), (uint16_t)(0x3u << my_leader));
             } else {
               mma_commit(empty_bar(stage));
               if (kb == num_k - 1) mma_commit(tfull_bar(acc));
@@ -276,13 +302,13 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int ew = warp - 2;                        // epilogue warp index (staging buffers)
     const uint32_t lane = lane_id();
     const uint32_t stage_base = sbase + C::STAGES * C::STAGE_BYTES + ew * 2 * C::EPI_BUF;
-    const uint32_t tempty_leader0 = (CG == 2) ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
+    const uint32_t tempty_leader0 = (CG == 2) ? map_to_rank(tempty_bar(0), my_leader) : tempty_bar(0);
     int acc = 0;
     uint32_t acc_phase = 0;
     int buf = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const TileCoord tc = sched.decode(t);
-      const int row0 = tc.mt * BM_CTA * CG + (int)rank * BM_CTA + q * 32;  // row in the C map
+      const int row0 = (tc.mt * PAIRS + pair) * BM_CTA * CG + (int)rank * BM_CTA + q * 32;  // C-map row
       const int col0 = tc.nt * BN;
       const CUtensorMap *cmap = sched.c_map(&tmC, tc.e);
       mbar_wait(tfull_bar(acc), acc_phase, 4);
@@ -356,25 +382,36 @@ template <int CG, bool B_MN, typename OutT, typename Prob>
 cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CUtensorMap &tC, int n,
                           int k, const Prob &prob, int tiles, int max_clusters, cudaStream_t stream) {
   using C = Cfg<CG, B_MN, OutT>;
-  int clusters = sm_count() / CG;
-  if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
-  if (clusters > tiles) clusters = tiles;
-  if (clusters <= 0) return cudaSuccess;
+  constexpr int CS = CG * Prob::kPairs;  // CTAs per cluster
   auto kern = gemm_bf16_kernel<CG, B_MN, OutT, Prob>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CG, 1, 1);
   cfg.blockDim = dim3(NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be co-resident (GPC packing may
+  // leave SMs idle for clusters > 2), never more than there are tiles
+  int clusters = sm_count() / CS;
+  {
+    cfg.gridDim = dim3(clusters * CS, 1, 1);
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0 &&
+        active < clusters)
+      clusters = active;
+    cudaGetLastError();
+  }
+  if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
+  if (clusters > tiles) clusters = tiles;
+  if (clusters <= 0) return cudaSuccess;
+  cfg.gridDim = dim3(clusters * CS, 1, 1);
   return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, prob);
 }
 
@@ -396,10 +433,24 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
                         : make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, g.ldb,
                                        BK, C::NB_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tC = make_c_map<OutT>(g.c, g.m, g.n, g.ldc);
+  const int mt = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
+  const int num_n = (int)((g.n + BN - 1) / BN);
+  const int group = g.raster_group > 0 ? g.raster_group : 8;
+  if constexpr (CG == 2) {
+    if (g.cluster_pairs == 2) {
+      SchedT<2> s;
+      s.num_m = (mt + 1) / 2;
+      s.num_n = num_n;
+      s.group = (group + 1) / 2;
+      s.M = (int)g.m;
+      return launch_kernel<CG, B_MN, OutT>(tA, tB, tC, (int)g.n, (int)g.k, s, s.num_m * s.num_n,
+                                           g.max_clusters, stream);
+    }
+  }
   Sched s;
-  s.num_m = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
-  s.num_n = (int)((g.n + BN - 1) / BN);
-  s.group = g.raster_group > 0 ? g.raster_group : 8;
+  s.num_m = mt;
+  s.num_n = num_n;
+  s.group = group;
   s.M = (int)g.m;
   return launch_kernel<CG, B_MN, OutT>(tA, tB, tC, (int)g.n, (int)g.k, s, s.num_m * s.num_n,
                                        g.max_clusters, stream);

@@ -64,7 +64,7 @@ def _dev_case(m, k, n, seed):
     return a, b, ta, tb
 
 
-@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("cta_group", [1, 2, 4])
 @pytest.mark.parametrize("b_layout", ["kn", "nk"])
 @pytest.mark.parametrize("out", ["f32", "bf16"])
 def test_device_gemm_1024_full_oracle(P, cta_group, b_layout, out):
@@ -98,7 +98,7 @@ def _full_oracle_1024(a, b):
 
 @pytest.mark.parametrize("m,k,n", [(1, 8, 8), (130, 72, 264), (384, 1000, 520), (257, 4104, 136),
                                    (2048, 64, 2048)])
-@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("cta_group", [1, 2, 4])
 def test_device_gemm_ragged(P, m, k, n, cta_group):
     import torch
     a, b, ta, tb = _dev_case(m, k, n, m + n + k)

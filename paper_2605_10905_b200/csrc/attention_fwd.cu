@@ -52,6 +52,11 @@ constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K (K-
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);    // P (TMEM) x V (MN-major)
 constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 256;       // TMEM column bases
 constexpr float LOG2E = 1.4426950408889634f;
+#ifdef MIMW_FA_SPIN
+#define MMA_WAIT mbar_wait_spin
+#else
+#define MMA_WAIT mbar_wait
+#endif
 constexpr int kDefaultEmu = 2;  // exp2 pairs (of 8) evaluated on the FMA pipe
 constexpr int HEAD_BAND = 4;    // heads per scheduling band (K/V of a band stays in L2)
 
@@ -186,6 +191,17 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
   const int num_items = p.bh * p.nqb;
+#ifdef MIMW_FA_EVENTS
+  // event log of CTA 0 (tools/fa_events.py): warps 0, 4 (softmax lane quarter 0) and 9 (MMA)
+  int ev_n = 0;
+#define EV(code)                                                                          \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && lane == 0 && ev_n < 1024 && p.trace)                           \
+      p.trace[warp * 1024 + ev_n++] = ((unsigned long long)clock64() << 8) | (code);     \
+  } while (0)
+#else
+#define EV(code) do {} while (0)
+#endif
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -198,7 +214,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       mbar_init(p_full(h), 4);
       mbar_init(o_done(h), 1);
       mbar_init(sched_full(h), 1);
-      mbar_init(sched_empty(h), 9);  // MMA thread + 8 softmax warps
+      mbar_init(sched_empty(h), 10);  // 2 MMA warps + 8 softmax warps
     }
     mbar_init(s_free, 4);
     for (int s = 0; s < NSLOT; ++s) {
@@ -263,10 +279,11 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         }
       }
     }
-  } else if (warp == 9) {
-    // ================= MMA issuer =================
+  } else if (warp == 9 || warp == 10) {
+    // ================= MMA issuers (S: warp 9, PV: warp 10) =================
     // The whole warp runs the schedule (so descriptor math stays on the
     // uniform datapath); one elected lane issues tcgen05.mma / commit.
+    const bool s_role = warp == 9;
     uint32_t ring = 0;  // K/V ring positions consumed so far (K_j at 2(j-lo), V_j at 2(j-lo)+1)
     uint32_t q_phase = 0, sf_phase = 0;
     uint32_t p_phase0 = 0, p_phase1 = 0;
@@ -275,9 +292,26 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO, version, SW128
     constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;                         // LBO (unused)
     constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;         // LBO = D-panel stride
-    auto ring_wait = [&](uint32_t pos) { mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 23); };
+#ifdef MIMW_FA_TRACE
+    long long mt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define MIMW_TR_BEGIN const long long _t0 = clock64();
+#define MIMW_TR_END(i) mt_acc[i] += clock64() - _t0;
+#else
+#define MIMW_TR_BEGIN
+#define MIMW_TR_END(i)
+#endif
+    auto ring_wait = [&](uint32_t pos) {
+      MIMW_TR_BEGIN
+      MMA_WAIT(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 23);
+      MIMW_TR_END(2)
+    };
     auto issue_S = [&](int h, uint32_t kslot) {
-      mbar_wait(s_free, sf_phase ^ 1, 24);  // S buffer released by its last reader
+      {
+        MIMW_TR_BEGIN
+        MMA_WAIT(s_free, sf_phase ^ 1, 24);  // S buffer released by its last reader
+        MIMW_TR_END(3)
+      }
+      EV(1 + 2 * h);
       sf_phase ^= 1;
       tc_fence_after();
       const uint32_t qa = (sb + SMEM_Q + h * TILE_BYTES) >> 4;
@@ -292,9 +326,15 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mma_commit(s_full(h));
       }
       __syncwarp();
+      EV(21 + 2 * h);
     };
     auto issue_PV = [&](int h, uint32_t vslot, bool acc) {
-      mbar_wait(p_full(h), h ? p_phase1 : p_phase0, 25 + h);
+      {
+        MIMW_TR_BEGIN
+        MMA_WAIT(p_full(h), h ? p_phase1 : p_phase0, 25 + h);
+        MIMW_TR_END(h)
+      }
+      EV(2 + 2 * h);
       if (h) p_phase1 ^= 1; else p_phase0 ^= 1;
       tc_fence_after();
       const uint32_t vb = (sb + SMEM_KV + vslot * TILE_BYTES) >> 4;
@@ -307,6 +347,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mma_commit(o_done(h));
       }
       __syncwarp();
+      EV(22 + 2 * h);
     };
     auto release = [&](uint32_t slot) {
       if (elect_one()) mma_commit(kv_empty(slot));
@@ -328,31 +369,42 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       const bool has1 = r0 + BQ < p.seq;
       if (!has1) hi1 = hi0;
       const int lo = min(lo0, lo1), hi = max(hi0, hi1);
-      mbar_wait(q_full(0), q_phase, 21);
-      mbar_wait(q_full(1), q_phase, 22);
+      if (s_role) {
+        MIMW_TR_BEGIN
+        mbar_wait(q_full(0), q_phase, 21);
+        mbar_wait(q_full(1), q_phase, 22);
+        MIMW_TR_END(6)
+      }
       q_phase ^= 1;
-      for (int j = lo; j <= hi + 1; ++j) {
+      // Two issuers keep the tensor pipe fed: tcgen05.mma issue blocks at the
+      // pipe rate, so while one warp waits on a dependency the other's group
+      // is already queued.  Warp 9 issues every S = Q K^T (and releases K
+      // slots), warp 10 every O += P V (and releases V slots).
+      for (int j = lo; j <= hi; ++j) {
         const uint32_t kpos = ring + 2 * (j - lo);
-        const uint32_t vpos = kpos - 1;  // V_{j-1}
-        if (j <= hi) {
+        if (s_role) {
           ring_wait(kpos);
           if (j >= lo0 && j <= hi0) issue_S(0, kpos % NSLOT);
-        }
-        if (j > lo) {
-          ring_wait(vpos);
-          if (j - 1 >= lo0 && j - 1 <= hi0) issue_PV(0, vpos % NSLOT, j - 1 != lo0);
-        }
-        if (j <= hi) {
           if (has1 && j >= lo1 && j <= hi1) issue_S(1, kpos % NSLOT);
           release(kpos % NSLOT);  // K_j: both S products issued
-        }
-        if (j > lo) {
-          if (has1 && j - 1 >= lo1 && j - 1 <= hi1) issue_PV(1, vpos % NSLOT, j - 1 != lo1);
-          release(vpos % NSLOT);  // V_{j-1}
+        } else {
+          const uint32_t vpos = kpos + 1;  // V_j
+          ring_wait(vpos);
+          EV(20);
+          if (j >= lo0 && j <= hi0) issue_PV(0, vpos % NSLOT, j != lo0);
+          if (has1 && j >= lo1 && j <= hi1) issue_PV(1, vpos % NSLOT, j != lo1);
+          release(vpos % NSLOT);  // V_j
         }
       }
       ring += 2 * (hi - lo + 1);
+#ifdef MIMW_FA_TRACE
+      mt_acc[4] += hi - lo + 1;
+#endif
     }
+#ifdef MIMW_FA_TRACE
+    if (p.trace && lane == 0)
+      for (int e = 0; e < 8; ++e) p.trace[((size_t)blockIdx.x * 12 + warp) * 8 + e] = mt_acc[e];
+#endif
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
@@ -395,6 +447,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mbar_wait(s_full(h), s_phase, 30 + h);
         s_phase ^= 1;
         tc_fence_after();
+        EV(10);
 #ifdef MIMW_FA_TRACE
         const long long tr1 = clock64();
 #endif
@@ -419,6 +472,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           }
         }
         tmem_ld_wait();
+        EV(11);
         // S is in registers: hand the buffer back (and Q_h after its last S)
         tc_fence_before();
         __syncwarp();
@@ -478,6 +532,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           ++od_count;
           tc_fence_after();
         }
+        EV(13);
         if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll 1
           for (int c = 0; c < 128; c += 32) {
@@ -519,6 +574,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full(h));
+        EV(14);
 #ifdef MIMW_FA_TRACE
         {
           tr_acc[0] += tr1 - tr0;  // waiting for S

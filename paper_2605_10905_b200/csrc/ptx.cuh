@@ -152,6 +152,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
   }
 }
 
+// Non-suspending poll (mbarrier.test_wait): for a latency-critical waiter that
+// shares its SM sub-partition with busy warps.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity, int tag = 0) {
+  if (mbar_test_wait(bar, parity)) return;
+  uint64_t t0 = clock64();
+  while (!mbar_test_wait(bar, parity)) {
+    if (clock64() - t0 > MIMW_WATCHDOG_CYCLES) watchdog_trap(bar, parity, tag);
+  }
+}
+
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity, int tag = 0) {
   if (mbar_try_wait_cluster(bar, parity)) return;
   uint64_t t0 = clock64();

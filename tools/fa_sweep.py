@@ -6,7 +6,7 @@ import paper_2605_10905_b200 as P
 bh, s = int(sys.argv[1]) if len(sys.argv) > 1 else 128, 8192
 q, k, v = ((torch.rand((bh, 1, s, 128), device="cuda") * 2 - 1).bfloat16() for _ in range(3))
 flop = 4.0 * bh * 128 * s * s / 2
-for emu in (2, 0, 1, 2, 0, 1, 3, 2):
+for emu in [int(x) for x in sys.argv[2:]] or (2, 0, 1, 2, 0, 1, 3, 2):
     for _ in range(3):
         P.attention_fwd(q, k, v, emu=emu)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

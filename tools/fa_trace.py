@@ -38,4 +38,6 @@ print(f"softmax warp per tile (n={n:.0f}/warp): wait_S {sm[0]/n:.0f}  ld_S {sm[1
       f"max+exp {sm[2]/n:.0f}  wait_PV+rescale {sm[3]/n:.0f}  P store+arrive {sm[5]/n:.0f} cycles")
 nm = mma[4].item()
 print(f"MMA warp per KV step (n={nm:.0f}): wait_P0 {mma[0]/nm:.0f}  wait_P1 {mma[1]/nm:.0f}  "
-      f"wait_K {mma[2]/nm:.0f}  wait_Sfree {mma[3]/nm:.0f} cycles")
+      f"wait_KV {mma[2]/nm:.0f}  wait_Sfree {mma[3]/nm:.0f}  wait_Q {mma[6]/nm:.0f} cycles")
+print(f"cycles per KV step (kernel time x 1.9 GHz / steps per CTA): "
+      f"{ms * 1e-3 * 1.9e9 / nm:.0f} (MMA ideal 2048)")

@@ -524,6 +524,30 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 #ifdef MIMW_FA_TRACE
         const long long tr3 = clock64();
 #endif
+#ifdef MIMW_FA_TRACE
+        const long long tr4 = clock64();
+#endif
+        // exponentials first, into registers: they do not touch TMEM, so they
+        // overlap the tail of PV_h(j-1), which still reads P_h / writes O_h
+        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
+        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
+        uint64_t acc[4] = {0, 0, 0, 0};
+        uint32_t pk[64];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const int c = 2 * e;
+          // x = s * scale*log2e - m, two lanes per FFMA2
+          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
+          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
+          acc[e & 3] = f2_add(acc[e & 3], p2);
+          pk[e] = pack_bf16_2(p2);
+        }
+        {
+          float a0, a1, b0, b1;
+          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
+          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
+          l += (a0 + a1) + (b0 + b1);
+        }
         // PV_h(j-1) must be complete before P_h is overwritten / O_h rescaled.
         // o_done[h] can be at most one phase ahead of the one awaited here
         // (PV_h(j) needs this P), so the parity wait is unambiguous.
@@ -545,31 +569,9 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             tmem_st_32x32b_x16(t_o + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
           }
         }
-#ifdef MIMW_FA_TRACE
-        const long long tr4 = clock64();
-#endif
-        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
-        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
-        uint64_t acc[4] = {0, 0, 0, 0};
-        uint32_t pk[64];
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const int c = 2 * e;
-          // x = s * scale*log2e - m, two lanes per FFMA2
-          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sl2, nm2);
-          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
-          acc[e & 3] = f2_add(acc[e & 3], p2);
-          pk[e] = pack_bf16_2(p2);
-          // stream P_h(j) into TMEM 16 columns (32 keys) at a time
-          if ((e & 15) == 15)
-            tmem_st_32x32b_x16(t_p + (e - 15), *reinterpret_cast<uint32_t(*)[16]>(&pk[e - 15]));
-        }
-        {
-          float a0, a1, b0, b1;
-          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-          l += (a0 + a1) + (b0 + b1);
-        }
+        for (int c = 0; c < 64; c += 16)
+          tmem_st_32x32b_x16(t_p + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();

@@ -7,7 +7,7 @@
 #include "../paper_2605_10905_b200/csrc/ptx.cuh"
 using namespace mimw;
 
-template <int SHAPE>  // 0: 32x32b.x32, 1: 32x32b.x128 (one instruction for 128 columns)
+template <int SHAPE>  // 0: ld 32x32b.x32, 1: ld 4 x 32x32b.x32, 2: st 32x32b.x16 (P stores)
 __global__ void __launch_bounds__(256, 1) k(long long *out, int iters, int delay, int nw) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
@@ -31,13 +31,22 @@ __global__ void __launch_bounds__(256, 1) k(long long *out, int iters, int delay
         tmem_ld_wait();
         x += r[0] + r[31];
         n += 4096;
-      } else {
+      } else if (SHAPE == 1) {
         uint32_t r[32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(base + c * 32, r);
         tmem_ld_wait();
         x += r[0] + r[31];
         n += 16384;
+      } else {
+        uint32_t r[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) r[c] = x + c;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_st_32x32b_x16(base + 64 + c * 16, r);
+        tmem_st_wait();
+        x += 1;
+        n += 8192;
       }
       if (delay) { long long t = clock64(); while (clock64() - t < delay) {} }
     }
@@ -67,10 +76,10 @@ int main() {
   long long *d; cudaMalloc(&d, 148 * 16 + 8192);
   long long h[296];
   const int iters = 8192;
-  for (int shape = 0; shape < 2; ++shape)
+  for (int shape = 0; shape < 3; ++shape)
     for (int nw : {1, 3, 7})
       for (int delay : {0, 200, 800, 2000}) {
-        auto kern = shape == 0 ? k<0> : k<1>;
+        auto kern = shape == 0 ? k<0> : shape == 1 ? k<1> : k<2>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
         kern<<<148, 256, 40000>>>(d, iters, delay, nw);
         cudaError_t e = cudaDeviceSynchronize();
@@ -78,7 +87,8 @@ int main() {
         double cyc = 0, ld = 0;
         for (int i = 0; i < 148; ++i) { cyc += h[2 * i]; ld += h[2 * i + 1]; }
         cyc /= 148; ld /= 148;
-        printf("%s nw %d delay %4d: %.1f cycles/MMA, LDTM %.1f B/clk/SM %s\n", shape ? "x128" : "x32 ", nw,
+        printf("%s nw %d delay %4d: %.1f cycles/MMA, TMEM ld/st %.1f B/clk/SM %s\n",
+               shape == 0 ? "ld x32 " : shape == 1 ? "ld x128" : "st x16 ", nw,
                delay, cyc / iters, ld / cyc, e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
   return 0;

@@ -14,8 +14,12 @@
 //   WG2 warp 8       TMA producer + tile scheduler (atomic work counter,
 //                    published through a 2-slot mbarrier ring: the CLC
 //                    clc_producer/clc_consumer protocol of sim.cpp:1213-1286)
-//   WG2 warp 9       MMA issuer: S = Q_h K_j^T (SS) and O_h += P_h V_j (TS)
-//   WG2 warps 10-11  idle (donate registers via setmaxnreg)
+//   WG2 warp 9       MMA issuer for S = Q_h K_j^T (SS), releases K slots
+//   WG2 warp 10      MMA issuer for O_h += P_h V_j (TS), releases V slots.
+//                    tcgen05.mma issue blocks at the tensor-pipe rate, so a
+//                    single issuer drains the pipe at every dependency wait
+//                    (measured: tools/fa_events.py); two keep it fed.
+//   WG2 warp 11      idle (donates registers via setmaxnreg)
 //
 // TMEM (512 columns x 128 lanes): S [0,128) fp32 (ONE buffer shared by both
 // Q tiles), P_0 [128,192) P_1 [192,256) bf16, O_0 [256,384) O_1 [384,512).
@@ -57,7 +61,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 #else
 #define MMA_WAIT mbar_wait
 #endif
-constexpr int kDefaultEmu = 2;  // exp2 pairs (of 8) evaluated on the FMA pipe
+constexpr int kDefaultEmu = 0;  // exp2 pairs (of 8) evaluated on the FMA pipe (0: measured fastest, tools/fa_sweep.py)
 constexpr int HEAD_BAND = 4;    // heads per scheduling band (K/V of a band stays in L2)
 
 struct Params {

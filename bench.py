@@ -527,6 +527,49 @@ def bench_moe(args, rank, ws, local):
             "gpu_launches": steps, "clocks": clocks}
 
 
+def bench_layernorm(args, rank, ws, local):
+    """cluster LayerNorm, PAPER.md:736 LN6 (1152 x 65536
+    f32), rows split across ranks; HBM-bound: 4 B read + 4 B written per element."""
+    import torch
+    import paper_2605_10905_b200 as P
+    L = P.lib()
+    pk = peaks()
+    dev = torch.device("cuda", local)
+    rows_total, n = 1152, 65536
+    from paper_2605_10905_b200 import shard
+    r0, r1 = shard.split_even(rows_total, ws)[rank]
+    rows = r1 - r0
+    g = torch.Generator(device=dev).manual_seed(5 + rank)
+    x = torch.randn((max(1, rows), n), device=dev, generator=g)
+    w = torch.randn(n, device=dev, generator=g)
+    b = torch.randn(n, device=dev, generator=g)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def step():
+        P._check(L.mimw_b200_layernorm(x.data_ptr(), w.data_ptr(), b.data_ptr(), y.data_ptr(), None,
+                                       None, rows, n, 1e-5, sptr))
+
+    steps = max(10, args.steps)
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(step, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    per = secs / steps
+    gbs = 8.0 * rows * n / per / 1e9
+    return {"value": round(8.0 * rows_total * n * steps / secs / 1e9, 1), "unit": "GB/s",
+            "ms_per_step": round(per * 1e3, 4), "scaling": "strong",
+            "config": {"workload": "cluster LayerNorm (SURVEY §8f rank 3), PAPER.md:736 LN6 "
+                                   "1152 x 65536 f32, one CTA cluster per row, DSM exchange",
+                       "l2": "x, y 2 x 302 MB > L2"},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"],
+                         "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
+                         "peak_source": f"{pk['src']} HBM copy bandwidth",
+                         "algorithmic_bytes_per_launch": 8.0 * rows * n, "traffic": None},
+            "clocks": clocks}
+
+
 def torch_empty_cache():
     import torch
     torch.cuda.empty_cache()
@@ -538,7 +581,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe"])
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -580,6 +623,8 @@ def main():
         res = bench_mxfp8(args, rank, ws, local)
     elif args.workload == "moe":
         res = bench_moe(args, rank, ws, local)
+    elif args.workload == "layernorm":
+        res = bench_layernorm(args, rank, ws, local)
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
@@ -593,6 +638,8 @@ def main():
             res["secondary"]["grouped_moe_gemm"] = {k: moe[k] for k in (
                 "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks",
                 "reassembly")}
+            torch_empty_cache()
+            res["secondary"]["layernorm_cluster"] = bench_layernorm(args, rank, ws, local)
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

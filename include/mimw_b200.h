@@ -116,6 +116,22 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
                             int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
                             int64_t window, double scale, void *stream);
 
+/* ---- Cluster LayerNorm ------------------------------
+ * Replaces: void oracle_layernorm(const Tile &x, const Tile &w, const Tile &b,
+ *                                 double eps, Tile *y, Tile *mean, Tile *rstd)
+ *           proj/core/src/oracles.cpp:28-55 (two-pass mean / variance), the
+ *           computation proj/kernels/layernorm_cluster.mimw:1-62 distributes
+ *           over a CTA cluster.  Host f32 buffers x[rows*n], w[n], b[n],
+ *           y[rows*n]; mean / rstd [rows] may be NULL.  n <= 262144. */
+int mimw_b200_oracle_layernorm(const float *x, const float *w, const float *b, double eps, float *y,
+                               float *mean, float *rstd, int64_t rows, int64_t n);
+
+/* Device form: f32 [rows, n] row-major; one thread-block cluster per row
+ * (CTA slices of <= 16K columns), partial reductions exchanged through
+ * distributed shared memory (st.async + remote mbarrier complete_tx). */
+int mimw_b200_layernorm(const float *x, const float *w, const float *b, float *y, float *mean,
+                        float *rstd, int64_t rows, int64_t n, double eps, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,9 @@ def _optional_sigs():
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
                                                                            C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
+        "mimw_b200_oracle_layernorm": [_fp, _fp, _fp, C.c_double, _fp, _fp, _fp, _i64, _i64],
+        "mimw_b200_layernorm": [_vp] * 6 + [_i64, _i64, C.c_double, _vp],
+        "mimw_b200_layernorm_ex": [_vp] * 6 + [_i64, _i64, C.c_double, C.c_int32, _vp],
         "mimw_b200_gemm_mxfp8_ex": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16_ex": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32,
@@ -140,6 +143,19 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
     return (o, lse) if with_lse else o
 
 
+def oracle_layernorm(x, w, b, eps: float):
+    """``oracle_layernorm(x, w, b, eps, &y, &mean, &rstd)`` (oracles.cpp:28-55)
+    on the B200 cluster kernel; returns (y, mean, rstd)."""
+    x, w, b = map(_f32, (x, w, b))
+    rows, n = x.shape
+    y = np.empty_like(x)
+    mean = np.empty(rows, np.float32)
+    rstd = np.empty(rows, np.float32)
+    _check(lib().mimw_b200_oracle_layernorm(_ptr(x), _ptr(w), _ptr(b), eps, _ptr(y), _ptr(mean),
+                                            _ptr(rstd), rows, n))
+    return y, mean, rstd
+
+
 def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: int = PREC_BF16):
     """``run_oracle`` (oracles.cpp:147-201) dispatching to the B200 path for
     the hot-path oracles.  Unknown / off-path names return ``None``."""
@@ -149,6 +165,9 @@ def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: 
     if name == "multi_device_gemm":
         return {"c": oracle_multi_device_gemm(inputs["a0"], inputs["a1"], inputs["b0"],
                                               inputs["b1"], precision)}
+    if name == "layernorm":
+        return {"y": oracle_layernorm(inputs["x"], inputs["w"], inputs["b"],
+                                      scalars.get("eps", 1e-5))[0]}
     if name == "attention":
         return {"o": oracle_attention(inputs["q"], inputs["k"], inputs["v"],
                                       int(scalars.get("w", 1 << 30)), scalars.get("scale", 1.0))}
@@ -244,4 +263,20 @@ def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, c
     _check(lib().mimw_b200_grouped_gemm_bf16_ex(x.data_ptr(), offs.ctypes.data, w.data_ptr(),
                                                 out.data_ptr(), g, n, k, w_layout, cta_group,
                                                 max_clusters, _stream(stream)))
+    return out
+
+
+def layernorm(x, w, b, eps: float = 1e-5, out=None, mean=None, rstd=None, stream=None,
+              cluster: int = 0):
+    """Cluster LayerNorm over the last dim of an f32 CUDA tensor [rows, n]."""
+    import torch
+    if x.dtype != torch.float32 or not x.is_contiguous():
+        raise MimwError(ERR_UNSUPPORTED, "layernorm needs a contiguous float32 tensor")
+    rows, n = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    _check(lib().mimw_b200_layernorm_ex(x.data_ptr(), w.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                        mean.data_ptr() if mean is not None else None,
+                                        rstd.data_ptr() if rstd is not None else None, rows, n,
+                                        eps, cluster, _stream(stream)))
     return out

@@ -19,6 +19,7 @@
 #include "attention_fwd.h"
 #include "gemm_bf16.h"
 #include "gemm_mxfp8.h"
+#include "layernorm_cluster.h"
 
 namespace {
 
@@ -253,6 +254,15 @@ void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *
   check_cuda(mimw::grouped_gemm_bf16_launch(g, stream), "grouped gemm launch");
 }
 
+void layernorm_checks(const void *x, const void *w, const void *b, const void *y, int64_t rows,
+                      int64_t n) {
+  require(rows >= 0 && n >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(n <= 16 * 16 * 1024, MIMW_ERR_UNSUPPORTED, "row length > 262144 not supported");
+  require(rows < (1ll << 31), MIMW_ERR_UNSUPPORTED, "rows >= 2^31");
+  if (rows == 0 || n == 0) return;
+  require(x && w && b && y, MIMW_ERR_ARG, "null pointer");
+}
+
 }  // namespace
 
 extern "C" {
@@ -402,6 +412,53 @@ int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const v
                                 void *stream) {
   return guarded([&] {
     grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mimw_b200_layernorm(const float *x, const float *w, const float *b, float *y, float *mean,
+                        float *rstd, int64_t rows, int64_t n, double eps, void *stream) {
+  return guarded([&] {
+    layernorm_checks(x, w, b, y, rows, n);
+    if (rows == 0 || n == 0) return;
+    require_sm100();
+    mimw::LayerNormArgs a{x, w, b, y, mean, rstd, rows, n, eps, 0};
+    check_cuda(mimw::layernorm_cluster_launch(a, static_cast<cudaStream_t>(stream)), "layernorm launch");
+  });
+}
+
+// Test hook (not part of the public header): LayerNorm with a forced cluster size.
+int mimw_b200_layernorm_ex(const float *x, const float *w, const float *b, float *y, float *mean,
+                           float *rstd, int64_t rows, int64_t n, double eps, int32_t cluster,
+                           void *stream) {
+  return guarded([&] {
+    layernorm_checks(x, w, b, y, rows, n);
+    require(cluster >= 0 && cluster <= 16, MIMW_ERR_ARG, "cluster must be 0..16");
+    if (rows == 0 || n == 0) return;
+    require_sm100();
+    mimw::LayerNormArgs a{x, w, b, y, mean, rstd, rows, n, eps, cluster};
+    check_cuda(mimw::layernorm_cluster_launch(a, static_cast<cudaStream_t>(stream)), "layernorm launch");
+  });
+}
+
+int mimw_b200_oracle_layernorm(const float *x, const float *w, const float *b, double eps, float *y,
+                               float *mean, float *rstd, int64_t rows, int64_t n) {
+  return guarded([&] {
+    layernorm_checks(x, w, b, y, rows, n);
+    if (rows == 0 || n == 0) return;
+    require_sm100();
+    cudaStream_t s = cudaStreamPerThread;
+    const size_t xn = (size_t)rows * n;
+    DevBuf dx(4 * xn, s), dw(4 * n, s), db(4 * n, s), dy(4 * xn, s), dm(4 * rows, s), dr(4 * rows, s);
+    check_cuda(cudaMemcpyAsync(dx.p, x, 4 * xn, cudaMemcpyHostToDevice, s), "H2D x");
+    check_cuda(cudaMemcpyAsync(dw.p, w, 4 * n, cudaMemcpyHostToDevice, s), "H2D w");
+    check_cuda(cudaMemcpyAsync(db.p, b, 4 * n, cudaMemcpyHostToDevice, s), "H2D b");
+    mimw::LayerNormArgs a{dx.as<float>(), dw.as<float>(), db.as<float>(), dy.as<float>(),
+                          dm.as<float>(), dr.as<float>(), rows, n, eps, 0};
+    check_cuda(mimw::layernorm_cluster_launch(a, s), "layernorm launch");
+    check_cuda(cudaMemcpyAsync(y, dy.p, 4 * xn, cudaMemcpyDeviceToHost, s), "D2H y");
+    if (mean) check_cuda(cudaMemcpyAsync(mean, dm.p, 4 * rows, cudaMemcpyDeviceToHost, s), "D2H mean");
+    if (rstd) check_cuda(cudaMemcpyAsync(rstd, dr.p, 4 * rows, cudaMemcpyDeviceToHost, s), "D2H rstd");
+    check_cuda(cudaStreamSynchronize(s), "layernorm execution");
   });
 }
 

@@ -80,7 +80,7 @@ def _optional_sigs():
         "mimw_b200_gemm_mxfp8_ex": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16_ex": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32,
-                                           C.c_int32, C.c_int32, _vp],
+                                           C.c_int32, C.c_int32, C.c_int32, _vp],
     }
 
 
@@ -240,7 +240,7 @@ def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None, cta_group: int = 2):
 
 
 def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, cta_group: int = 2,
-                 max_clusters: int = 0):
+                 max_clusters: int = 0, swap_tails: bool = True):
     """Grouped (MoE) GEMM: for each group e, ``out[off[e]:off[e+1]] =
     x[off[e]:off[e+1]] @ W_e`` with bf16 x [rows, K], w [G, K, N] (B_KN) or
     [G, N, K] (B_NK) CUDA tensors and ``m_offsets`` a host sequence of G+1
@@ -262,7 +262,8 @@ def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, c
         out = torch.empty((x.shape[0], n), device=x.device, dtype=torch.bfloat16)
     _check(lib().mimw_b200_grouped_gemm_bf16_ex(x.data_ptr(), offs.ctypes.data, w.data_ptr(),
                                                 out.data_ptr(), g, n, k, w_layout, cta_group,
-                                                max_clusters, _stream(stream)))
+                                                max_clusters, 1 if swap_tails else 0,
+                                                _stream(stream)))
     return out
 
 

@@ -222,7 +222,7 @@ void host_attention(const float *q, const float *k, const float *v, float *o, fl
 
 void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *y, int64_t n_groups,
                   int64_t n, int64_t k, int32_t w_layout, int cta_group, int max_clusters,
-                  cudaStream_t stream) {
+                  bool swap_tails, cudaStream_t stream) {
   require(w_layout == MIMW_B_KN || w_layout == MIMW_B_NK, MIMW_ERR_ARG, "bad w_layout");
   require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
   require(n_groups >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
@@ -251,6 +251,7 @@ void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *
   g.w_kn = w_layout == MIMW_B_KN;
   g.cta_group = cta_group;
   g.max_clusters = max_clusters;
+  g.swap_tails = swap_tails;
   check_cuda(mimw::grouped_gemm_bf16_launch(g, stream), "grouped gemm launch");
 }
 
@@ -411,7 +412,8 @@ int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const v
                                 int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
                                 void *stream) {
   return guarded([&] {
-    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, static_cast<cudaStream_t>(stream));
+    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, true,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -466,10 +468,11 @@ int mimw_b200_oracle_layernorm(const float *x, const float *w, const float *b, d
 // cta_group / cluster cap.
 int mimw_b200_grouped_gemm_bf16_ex(const void *x, const int64_t *m_offsets, const void *w, void *y,
                                    int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
-                                   int32_t cta_group, int32_t max_clusters, void *stream) {
+                                   int32_t cta_group, int32_t max_clusters, int32_t swap_tails,
+                                   void *stream) {
   return guarded([&] {
     grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, cta_group, max_clusters,
-                 static_cast<cudaStream_t>(stream));
+                 swap_tails != 0, static_cast<cudaStream_t>(stream));
   });
 }
 

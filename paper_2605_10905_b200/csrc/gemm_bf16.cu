@@ -64,8 +64,10 @@ struct Cfg {
 // One output tile of a (possibly grouped) problem.  Row `mt * BM` of the
 // group starts at A row `row_base + mt * BM`; rows at or beyond `rows` are
 // not stored (C/Y map row extent).
+// swap_n > 0 marks a grouped tail tile computed with swapped operands
+// (Y^T = W^T X^T: M = 256 output columns, N = swap_n rows of the group).
 struct TileCoord {
-  int e, mt, nt, row_base, rows;
+  int e, mt, nt, row_base, rows, swap_n;
 };
 
 // Dense problem: one [M,K] x B -> [M,N]; grouped-rasterised tile order
@@ -89,6 +91,7 @@ struct SchedT {
     if (g & 1) c.nt = num_n - 1 - c.nt;  // boustrophedon: reuse the B panels still in L2
     c.row_base = 0;
     c.rows = M;
+    c.swap_n = 0;
     return c;
   }
   __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *tmC, int) const { return tmC; }
@@ -110,6 +113,7 @@ struct GroupedSched {
   int row_off[MAX_GROUPS];       // first row of group e in X / Y
   int rows[MAX_GROUPS];          // m_e
   int n_groups, num_n, bm;       // bm = rows per cluster tile (128 * CG)
+  int swap;                      // tail tiles (< bm rows) use swapped operands (CG == 2)
   __device__ __forceinline__ int num_tiles() const { return tile_off[n_groups]; }
   __device__ __forceinline__ TileCoord decode(int t) const {
     int lo = 0, hi = n_groups - 1;  // last e with tile_off[e] <= t
@@ -119,13 +123,16 @@ struct GroupedSched {
     }
     const int e = lo;
     const int r = t - tile_off[e];
-    const int mtiles = (rows[e] + bm - 1) / bm;
+    const int full = rows[e] / bm;
+    const int tail = rows[e] - full * bm;
+    const int mtiles = full + (tail > 0);
     TileCoord c;
     c.e = e;
     c.mt = r % mtiles;
     c.nt = r / mtiles;
     c.row_base = row_off[e];
     c.rows = rows[e];
+    c.swap_n = (swap && c.mt == full && tail > 0) ? ((tail + 31) & ~31) : 0;
     return c;
   }
   __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *, int e) const { return &y[e]; }
@@ -193,7 +200,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), my_leader) : full_bar(0);
       for (int t = cluster; t < num_tiles; t += nclusters) {
         const TileCoord tc = sched.decode(t);
-        const int m0 = tc.row_base + (tc.mt * PAIRS + pair) * BM_CTA * CG + (int)rank * BM_CTA;
+        // swapped tail tile: this CTA stages rows [swap_n/2 * rank, +swap_n/2) of the
+        // group's tail as the MMA's B operand (same 128-row box; extra rows unused)
+        const int m0 = tc.row_base + (tc.mt * PAIRS + pair) * BM_CTA * CG +
+                       (int)rank * (tc.swap_n ? tc.swap_n / 2 : BM_CTA);
         const int n0 = tc.nt * BN + (int)rank * C::NB_CTA;
         for (int kb = 0; kb < num_k; ++kb) {
           if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
@@ -260,6 +270,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
+        int swap_n = 0;
+        if constexpr (GROUPED) swap_n = sched.decode(t).swap_n;
+        // swapped tail: A = W^T (the B slot, MN-major for [G,K,N]), B = X rows (the A slot)
+        const uint32_t idesc = swap_n ? idesc_bf16(BM_CTA * CG, swap_n, B_MN ? 1 : 0, 0) : C::IDESC;
         mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1, 2);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -279,7 +293,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               const uint64_t a_k = adesc + (uint64_t)((k * UMMA_K * 2) >> 4);
               const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((k * UMMA_K * 128) >> 4)
                                                           : ((k * UMMA_K * 2) >> 4));
-              mma_f16_ss<CG>(d_tmem, a_k, b_k, C::IDESC, (kb | k) != 0);
+              if (GROUPED && swap_n) mma_f16_ss<CG>(d_tmem, b_k, a_k, idesc, (kb | k) != 0);
+              else mma_f16_ss<CG>(d_tmem, a_k, b_k, idesc, (kb | k) != 0);
             }
             if constexpr (CG == 2) {
               // a stage is free once every pair that received its B has consumed it
@@ -311,6 +326,50 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int row0 = (tc.mt * PAIRS + pair) * BM_CTA * CG + (int)rank * BM_CTA + q * 32;  // C-map row
       const int col0 = tc.nt * BN;
       const CUtensorMap *cmap = sched.c_map(&tmC, tc.e);
+      if (GROUPED && tc.swap_n) {
+        // swapped tail: TMEM lane = output column, TMEM column = group row.
+        // Transpose 32 x 32 chunks through the staging buffer (SWIZZLE_64B).
+        mbar_wait(tfull_bar(acc), acc_phase, 4);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+        const int feat0 = tc.nt * BN + (int)rank * BM_CTA + q * 32;
+        const int nch = tc.swap_n / EPI_COLS;
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + ch * EPI_COLS, v);
+          tmem_ld_wait();
+          if (ch == nch - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader0 + 8 * acc);
+          }
+          const int tok0 = tc.mt * BM_CTA * CG + ch * EPI_COLS;
+          if (tok0 < tc.rows && feat0 < N) {
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            const uint32_t sbuf = stage_base + buf * C::EPI_BUF;
+            const uint32_t cbyte = (lane & 7) * 2;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const uint32_t pc = (lane >> 3) ^ ((r >> 1) & 3);
+              const __nv_bfloat16 hv = __float2bfloat16_rn(__uint_as_float(v[r]));
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(sbuf + r * 64 + pc * 16 + cbyte),
+                           "h"(*reinterpret_cast<const uint16_t *>(&hv))
+                           : "memory");
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(cmap, sbuf, feat0, tok0);
+              bulk_commit();
+            }
+            buf ^= 1;
+          }
+        }
+        if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       mbar_wait(tfull_bar(acc), acc_phase, 4);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -477,6 +536,7 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
     gs->n_groups = cnt;
     gs->num_n = (int)((g.n + BN - 1) / BN);
     gs->bm = BM_CTA * CG;
+    gs->swap = (CG == 2 && g.swap_tails) ? 1 : 0;
     int tiles = 0;
     int first_live = -1;
     for (int i = 0; i < cnt; ++i) {

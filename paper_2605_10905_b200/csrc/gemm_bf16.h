@@ -33,6 +33,7 @@ struct GroupedGemmArgs {
   bool w_kn;
   int cta_group;
   int max_clusters;
+  bool swap_tails;  // each group's < 256-row tail as a swapped-operand tile (Y^T = W^T X^T)
 };
 
 cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stream);

@@ -18,8 +18,8 @@ for e in range(64):
     w[e] = (torch.rand((K, N), device="cuda") * 2 - 1).bfloat16()
 y = torch.empty((int(offs[-1]), N), device="cuda", dtype=torch.bfloat16)
 flop = 2.0 * offs[-1] * K * N
-for cg in [int(a) for a in sys.argv[1:]] or [2, 1, 2, 1]:
-    f = lambda: P.grouped_gemm(x, offs, w, out=y, cta_group=cg)
+for cg in [int(a) for a in sys.argv[1:]] or [2, 3, 2, 3]:  # 3 = cta_group 2 without swapped tails
+    f = lambda: P.grouped_gemm(x, offs, w, out=y, cta_group=min(cg, 2), swap_tails=cg != 3)
     for _ in range(3):
         f()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -285,34 +285,61 @@ gemm_mxfp8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 
 // Reorder natural [rows, kb] UE8M0 scales into per-tile atoms:
 //   atom(tile, g, half)[r*16 + c*4 + y] = sf[tile*rows_per_tile + half*128 + 32c + r, 4g + y]
-// (127 = 1.0 outside the matrix).  One CTA per (tile, half, 8 k-groups); each warp writes
-// whole 512-byte atoms, one 16-byte line (lane r: rows 32c + r, c = 0..3) per
-// thread, so the stores are coalesced and every input sector is consumed by
-// the CTA (the 8 warps walk 8 consecutive k-groups = 32 bytes of each row).
-__global__ void __launch_bounds__(256) sf_tile_kernel(const uint8_t *__restrict__ sf, int rows, int kb,
-                                                      int rows_per_tile, int halves, int kg,
-                                                      uint8_t *__restrict__ out) {
-  const int tile = blockIdx.x, half = blockIdx.y;
-  const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int local0 = half * 128 + r;
-  for (int g = blockIdx.z * 8 + w; g < kg; g += 8 * gridDim.z) {
-    uint32_t word[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int local = local0 + 32 * c;
-      const int row = tile * rows_per_tile + local;
-      uint32_t v = 0;
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const int k = 4 * g + y;
-        uint32_t b = 127;
-        if (local < rows_per_tile && row < rows && k < kb) b = __ldg(sf + (size_t)row * kb + k);
-        v |= b << (8 * y);
+// (127 = 1.0 outside the matrix), for SFA (128-row tiles, 1 half) and SFB
+// (224-row tiles, 2 halves) in ONE launch.  A CTA owns one 128-row group and
+// 32 k-groups: it reads the 128 x 128-byte block row-wise (coalesced) into
+// padded smem, then writes the 32 atoms as whole 512-byte lines.
+__global__ void __launch_bounds__(256) sf_tile_kernel(const uint8_t *__restrict__ sfa, int m,
+                                                      const uint8_t *__restrict__ sfb, int n, int kb,
+                                                      int kg, int m128, uint8_t *__restrict__ out_a,
+                                                      uint8_t *__restrict__ out_b) {
+  constexpr int PITCH = 33;  // words per smem row (+1: conflict-free column reads)
+  __shared__ uint32_t blk[128 * PITCH];
+  const int grp = blockIdx.x;
+  const bool is_a = grp < m128;
+  const uint8_t *sf = is_a ? sfa : sfb;
+  const int rows = is_a ? m : n;
+  int row0, valid;  // first row of the group, rows of the group inside its tile
+  uint8_t *out;
+  int halves, tile, half;
+  if (is_a) {
+    tile = grp; half = 0; halves = 1; row0 = grp * 128; valid = 128; out = out_a;
+  } else {
+    const int gg = grp - m128;
+    tile = gg >> 1; half = gg & 1; halves = 2;
+    row0 = tile * BN + half * 128; valid = min(128, BN - half * 128); out = out_b;
+  }
+  const int g0 = blockIdx.y * 32;
+  const int k0 = g0 * 4;  // first byte (k-block) of this chunk in a row
+  // load: 128 rows x 128 bytes, one byte-quad (4 k-blocks = one word) per load
+  for (int i = threadIdx.x; i < 128 * 32; i += 256) {
+    const int r = i >> 5, wq = i & 31;
+    const int row = row0 + r, k = k0 + wq * 4;
+    uint32_t v = 0x7F7F7F7Fu;
+    if (r < valid && row < rows) {
+      const uint8_t *src = sf + (size_t)row * kb + k;
+      if (k + 3 < kb && ((reinterpret_cast<uintptr_t>(src) & 3) == 0)) {
+        v = __ldg(reinterpret_cast<const uint32_t *>(src));
+      } else {
+        v = 0;
+        for (int y = 0; y < 4; ++y) v |= (uint32_t)(k + y < kb ? __ldg(src + y) : 127) << (8 * y);
       }
-      word[c] = v;
     }
+    blk[r * PITCH + wq] = v;
+  }
+  __syncthreads();
+  // write: atom (g0 + a) line r = words {blk[32c + r][a]}, c = 0..3
+  for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+    const int a = i >> 5, r = i & 31;
+    const int g = g0 + a;
+    if (g >= kg) continue;
+    uint4 w;
+    w.x = blk[(r) * PITCH + a];
+    w.y = blk[(32 + r) * PITCH + a];
+    w.z = blk[(64 + r) * PITCH + a];
+    w.w = blk[(96 + r) * PITCH + a];
     uint8_t *dst = out + ((size_t)((size_t)tile * kg + g) * halves + half) * 512 + r * 16;
-    *reinterpret_cast<uint4 *>(dst) = make_uint4(word[0], word[1], word[2], word[3]);
+    *reinterpret_cast<uint4 *>(dst) = w;
   }
 }
 
@@ -337,11 +364,9 @@ cudaError_t launch_cg(const Mxfp8Args &g, cudaStream_t stream) {
   uint8_t *sfa_t = static_cast<uint8_t *>(g.workspace);
   uint8_t *sfb_t = sfa_t + (size_t)m128 * kg * SFA_BYTES;
   const int kb = (int)(g.k / 32);
-  const int gz = (kg + 7) / 8;
-  sf_tile_kernel<<<dim3(m128, 1, gz), 256, 0, stream>>>(static_cast<const uint8_t *>(g.sfa), (int)g.m, kb,
-                                                    BM_CTA, 1, kg, sfa_t);
-  sf_tile_kernel<<<dim3(num_n, 2, gz), 256, 0, stream>>>(static_cast<const uint8_t *>(g.sfb), (int)g.n, kb,
-                                                     BN, 2, kg, sfb_t);
+  sf_tile_kernel<<<dim3(m128 + 2 * num_n, (kg + 31) / 32), 256, 0, stream>>>(
+      static_cast<const uint8_t *>(g.sfa), (int)g.m, static_cast<const uint8_t *>(g.sfb), (int)g.n, kb,
+      kg, m128, sfa_t, sfb_t);
   CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.m, g.k, g.lda, BK, BM_CTA,
                                 CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tB = make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.n, g.k, g.ldb, BK, Cf::NB_CTA,

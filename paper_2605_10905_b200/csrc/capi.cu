@@ -78,6 +78,29 @@ void require_pitch(const void *p, int64_t ld, int64_t es, const char *name) {
           std::string(name) + ": row pitch must be a multiple of 16 bytes (TMA)");
 }
 
+// RAII CUDA event (timing disabled).
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() { check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create"); }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  Event(const Event &) = delete;
+  Event &operator=(const Event &) = delete;
+  Event(Event &&o) noexcept : e(o.e) { o.e = nullptr; }
+};
+
+// Per-thread, per-device copy streams for the pipelined host-buffer entries.
+cudaStream_t side_stream(int which) {
+  thread_local cudaStream_t st[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!st[dev][which])
+    check_cuda(cudaStreamCreateWithFlags(&st[dev][which], cudaStreamNonBlocking), "stream create");
+  return st[dev][which];
+}
+
 // RAII device scratch on a stream.
 struct DevBuf {
   void *p = nullptr;
@@ -116,7 +139,11 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
     require(k_parts[i] == 0 || (a_parts[i] && b_parts[i]), MIMW_ERR_ARG, "null input");
   require_sm100();
 
+  // Pipelined over row chunks of A/C on three streams: H2D copies (cs),
+  // staging + GEMM (s), D2H copies (ds), so PCIe traffic in both directions
+  // overlaps the tensor-core work (the host-f32 Tile path is PCIe-bound).
   cudaStream_t s = cudaStreamPerThread;
+  cudaStream_t cs = side_stream(0), ds = side_stream(1);
   const int nseg = precision == MIMW_PREC_F32_BF16X3 ? 3 : 1;
   const int64_t kp = round_up(k, 8);  // bf16 row pitch multiple of 16 B
   const int64_t np = round_up(n, 8);
@@ -125,49 +152,89 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   for (size_t i = 0; i < a_parts.size(); ++i) in_elems += (m + n) * k_parts[i];
   DevBuf din(sizeof(float) * in_elems, s);
   DevBuf dA(2 * m * kt, s), dB(2 * kt * np, s), dC(sizeof(float) * m * np, s);
+  Event e_alloc, e_b;
+  check_cuda(cudaEventRecord(e_alloc.e, s), "event");
+  check_cuda(cudaStreamWaitEvent(cs, e_alloc.e, 0), "wait");
+  check_cuda(cudaStreamWaitEvent(ds, e_alloc.e, 0), "wait");
 
   // segment products: (A part, B part) for hi.hi [, hi.lo, lo.hi]
   const int a_part_of_seg[3] = {0, 0, 1};
   const int b_part_of_seg[3] = {0, 1, 0};
-  float *cursor = din.as<float>();
-  int64_t koff = 0;
-  for (size_t i = 0; i < a_parts.size(); ++i) {
-    const int64_t ki = k_parts[i];
-    if (ki == 0) continue;
-    float *da = cursor;
-    float *db = cursor + m * ki;
-    cursor += (m + n) * ki;
-    check_cuda(cudaMemcpyAsync(da, a_parts[i], sizeof(float) * m * ki, cudaMemcpyHostToDevice, s), "H2D a");
-    check_cuda(cudaMemcpyAsync(db, b_parts[i], sizeof(float) * ki * n, cudaMemcpyHostToDevice, s), "H2D b");
-    const bool last = (i + 1 == a_parts.size()) || (koff + ki == k);
-    for (int sgi = 0; sgi < nseg; ++sgi) {
-      const int64_t base = sgi * kp + koff;
-      // the last part also zero-fills the K padding of its segment
-      const int64_t a_pad = last ? (kp - koff) : ki;
-      mimw::stage_cols_bf16(da, m, ki, a_pad, dA.p, kt, base, a_part_of_seg[sgi], s);
-      mimw::stage_rows_bf16(db, ki, a_pad, n, np, dB.p, np, base, b_part_of_seg[sgi], s);
+  std::vector<float *> da(a_parts.size()), db(a_parts.size());
+  {
+    float *cursor = din.as<float>();
+    for (size_t i = 0; i < a_parts.size(); ++i) {
+      da[i] = cursor;
+      db[i] = cursor + m * k_parts[i];
+      cursor += (m + n) * k_parts[i];
     }
-    koff += ki;
   }
-  check_cuda(cudaGetLastError(), "staging kernels");
-
-  mimw::GemmArgs g{};
-  g.a = dA.p;
-  g.b = dB.p;
-  g.c = dC.p;
-  g.m = m;
-  g.n = np;
-  g.k = kt;
-  g.lda = kt;
-  g.ldb = np;
-  g.ldc = np;
-  g.b_kn = true;
-  g.c_f32 = true;
-  g.cta_group = 2;
-  check_cuda(mimw::gemm_bf16_launch(g, s), "gemm launch");
-  check_cuda(cudaMemcpy2DAsync(c, sizeof(float) * n, dC.p, sizeof(float) * np, sizeof(float) * n, m,
-                               cudaMemcpyDeviceToHost, s),
-             "D2H c");
+  // B (every part) first: all chunks need it
+  for (size_t i = 0; i < a_parts.size(); ++i)
+    if (k_parts[i])
+      check_cuda(cudaMemcpyAsync(db[i], b_parts[i], sizeof(float) * k_parts[i] * n,
+                                 cudaMemcpyHostToDevice, cs), "H2D b");
+  check_cuda(cudaEventRecord(e_b.e, cs), "event");
+  check_cuda(cudaStreamWaitEvent(s, e_b.e, 0), "wait");
+  {
+    int64_t koff = 0;
+    for (size_t i = 0; i < a_parts.size(); ++i) {
+      const int64_t ki = k_parts[i];
+      if (ki == 0) continue;
+      const bool last = (i + 1 == a_parts.size()) || (koff + ki == k);
+      const int64_t pad = last ? (kp - koff) : ki;  // the last part zero-fills the K padding
+      for (int sgi = 0; sgi < nseg; ++sgi)
+        mimw::stage_rows_bf16(db[i], ki, pad, n, np, dB.p, np, sgi * kp + koff, b_part_of_seg[sgi], s);
+      koff += ki;
+    }
+  }
+  const int64_t chunk = std::max<int64_t>(512, round_up((m + 7) / 8, 256));
+  const int nchunks = (int)((m + chunk - 1) / chunk);
+  std::vector<Event> e_a(nchunks), e_c(nchunks);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int64_t r0 = ci * chunk, rows = std::min(chunk, m - r0);
+    for (size_t i = 0; i < a_parts.size(); ++i)
+      if (k_parts[i])
+        check_cuda(cudaMemcpyAsync(da[i] + r0 * k_parts[i], a_parts[i] + r0 * k_parts[i],
+                                   sizeof(float) * rows * k_parts[i], cudaMemcpyHostToDevice, cs),
+                   "H2D a");
+    check_cuda(cudaEventRecord(e_a[ci].e, cs), "event");
+    check_cuda(cudaStreamWaitEvent(s, e_a[ci].e, 0), "wait");
+    char *dA_rows = static_cast<char *>(dA.p) + (size_t)r0 * kt * 2;
+    int64_t koff = 0;
+    for (size_t i = 0; i < a_parts.size(); ++i) {
+      const int64_t ki = k_parts[i];
+      if (ki == 0) continue;
+      const bool last = (i + 1 == a_parts.size()) || (koff + ki == k);
+      const int64_t pad = last ? (kp - koff) : ki;
+      for (int sgi = 0; sgi < nseg; ++sgi)
+        mimw::stage_cols_bf16(da[i] + r0 * ki, rows, ki, pad, dA_rows, kt, sgi * kp + koff,
+                              a_part_of_seg[sgi], s);
+      koff += ki;
+    }
+    check_cuda(cudaGetLastError(), "staging kernels");
+    mimw::GemmArgs g{};
+    g.a = dA_rows;
+    g.b = dB.p;
+    g.c = static_cast<char *>(dC.p) + (size_t)r0 * np * 4;
+    g.m = rows;
+    g.n = np;
+    g.k = kt;
+    g.lda = kt;
+    g.ldb = np;
+    g.ldc = np;
+    g.b_kn = true;
+    g.c_f32 = true;
+    g.cta_group = 2;
+    check_cuda(mimw::gemm_bf16_launch(g, s), "gemm launch");
+    check_cuda(cudaEventRecord(e_c[ci].e, s), "event");
+    check_cuda(cudaStreamWaitEvent(ds, e_c[ci].e, 0), "wait");
+    check_cuda(cudaMemcpy2DAsync(c + r0 * n, sizeof(float) * n, static_cast<char *>(dC.p) + (size_t)r0 * np * 4,
+                                 sizeof(float) * np, sizeof(float) * n, rows, cudaMemcpyDeviceToHost, ds),
+               "D2H c");
+  }
+  check_cuda(cudaStreamSynchronize(ds), "gemm execution");
+  check_cuda(cudaStreamSynchronize(cs), "gemm execution");
   check_cuda(cudaStreamSynchronize(s), "gemm execution");
 }
 

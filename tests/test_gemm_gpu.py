@@ -135,3 +135,19 @@ def test_k_zero_gives_zeros(P):
     out = torch.full((64, 64), 7.0, device="cuda")
     P.gemm(ta, tb, out=out)
     assert torch.count_nonzero(out).item() == 0
+
+
+@pytest.mark.parametrize("m,k,n", [(2000, 300, 264), (1537, 72, 40)])
+def test_host_path_pipelined_chunks(P, m, k, n):
+    """The host-f32 entry pipelines row chunks of 512+ rows over three
+    streams; results equal the oracle in both precisions."""
+    a = oracle.random_tile([m, k], oracle.input_seed(3, 0))
+    b = oracle.random_tile([k, n], oracle.input_seed(3, 1))
+    want = oracle.oracle_gemm(a, b)
+    assert oracle.rel_error(P.oracle_gemm(a, b, precision=P.PREC_F32_BF16X3), want) <= 1e-4
+    assert oracle.rel_error(P.oracle_gemm(a, b), want) <= BF16_TOL
+    a1 = oracle.random_tile([m, 40], oracle.input_seed(3, 2))
+    b1 = oracle.random_tile([40, n], oracle.input_seed(3, 3))
+    want = oracle.oracle_multi_device_gemm(a, a1, b, b1)
+    got = P.oracle_multi_device_gemm(a, a1, b, b1, precision=P.PREC_F32_BF16X3)
+    assert oracle.rel_error(got, want) <= 1e-4

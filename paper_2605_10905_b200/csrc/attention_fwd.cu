@@ -191,8 +191,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   const uint32_t tmem_slot = bars + 120 + 16 * NSLOT;
   volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 120 + 16 * NSLOT);
   volatile int *sched_slot = reinterpret_cast<int *>(smem + SMEM_BAR + 128 + 16 * NSLOT);  // [2]
-  // number of S groups issued so far (S issuer -> PV issuer, see below)
-  volatile int *s_count = reinterpret_cast<int *>(smem + SMEM_BAR + 136 + 16 * NSLOT);
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -223,7 +221,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       mbar_init(sched_empty(h), 10);  // 2 MMA warps + 8 softmax warps
     }
     mbar_init(s_free, 4);
-    *s_count = 0;
     for (int s = 0; s < NSLOT; ++s) {
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
@@ -294,7 +291,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     uint32_t ring = 0;  // K/V ring positions consumed so far (K_j at 2(j-lo), V_j at 2(j-lo)+1)
     uint32_t q_phase = 0, sf_phase = 0;
     uint32_t p_phase0 = 0, p_phase1 = 0;
-    int s_issued = 0;  // S issuer: groups issued; PV issuer: S groups of finished items
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t sb = __shfl_sync(0xffffffffu, sbase, 0);
     constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO, version, SW128
@@ -334,7 +330,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mma_commit(s_full(h));
       }
       __syncwarp();
-      if (lane == 0) *s_count = ++s_issued;
       EV(21 + 2 * h);
     };
     auto issue_PV = [&](int h, uint32_t vslot, bool acc) {
@@ -378,7 +373,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       const bool has1 = r0 + BQ < p.seq;
       if (!has1) hi1 = hi0;
       const int lo = min(lo0, lo1), hi = max(hi0, hi1);
-      const int item_s = (hi0 - lo0 + 1) + (has1 ? hi1 - lo1 + 1 : 0);  // S groups of this item
       if (s_role) {
         MIMW_TR_BEGIN
         mbar_wait(q_full(0), q_phase, 21);
@@ -401,33 +395,12 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           const uint32_t vpos = kpos + 1;  // V_j
           ring_wait(vpos);
           EV(20);
-          // Let the next S of the same Q tile into the tensor pipe first: PV_h(j)
-          // has ~2000 cycles of slack (P_h(j+1) is far off), while S_h(j+1) is
-          // on the S-buffer critical path (S0 -> load -> S1 -> load -> S0 ...).
-          auto s_target = [&](int h, int lo_h, int hi_h) {
-            if (j + 1 > hi_h) return s_issued + item_s;  // last PV of this tile: all S of the item
-            const int jj = j + 1;
-            const int c0 = max(0, min(jj, hi0 + 1) - lo0);
-            const int c1 = has1 ? max(0, min(jj, hi1 + 1) - lo1) : 0;
-            const int at = h == 0 ? 1 : ((jj >= lo0 && jj <= hi0) ? 1 : 0) + 1;
-            (void)lo_h;
-            return s_issued + c0 + c1 + at;
-          };
-          if (j >= lo0 && j <= hi0) {
-            const int tgt = s_target(0, lo0, hi0);
-            while (*s_count < tgt) __nanosleep(20);
-            issue_PV(0, vpos % NSLOT, j != lo0);
-          }
-          if (has1 && j >= lo1 && j <= hi1) {
-            const int tgt = s_target(1, lo1, hi1);
-            while (*s_count < tgt) __nanosleep(20);
-            issue_PV(1, vpos % NSLOT, j != lo1);
-          }
+          if (j >= lo0 && j <= hi0) issue_PV(0, vpos % NSLOT, j != lo0);
+          if (has1 && j >= lo1 && j <= hi1) issue_PV(1, vpos % NSLOT, j != lo1);
           release(vpos % NSLOT);  // V_j
         }
       }
       ring += 2 * (hi - lo + 1);
-      if (!s_role) s_issued += item_s;
 #ifdef MIMW_FA_TRACE
       mt_acc[4] += hi - lo + 1;
 #endif

@@ -1,0 +1,34 @@
+"""Small invocations of every kernel, for compute-sanitizer (racecheck /
+synccheck / memcheck) runs — the GPU analogue of the reference simulator's
+vector-clock race detector (sim.cpp:282-316):
+    compute-sanitizer --tool racecheck python tools/sanitize.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_10905_b200 as P  # noqa: E402
+
+torch.manual_seed(0)
+a = torch.randn(300, 200, device="cuda").bfloat16()
+b = torch.randn(200, 264, device="cuda").bfloat16()
+for cg in (1, 2, 4):
+    P.gemm(a, b, cta_group=cg)
+q, k, v = (torch.randn(1, 2, 300, 128, device="cuda").bfloat16() for _ in range(3))
+P.attention_fwd(q, k, v)
+P.attention_fwd(q, k, v, window=77)
+offs = np.array([0, 5, 5, 300, 400], np.int64)
+x = torch.randn(400, 128, device="cuda").bfloat16()
+w = torch.randn(4, 128, 264, device="cuda").bfloat16()
+P.grouped_gemm(x, offs, w)
+P.grouped_gemm(x, offs, w, swap_tails=False)
+qa = torch.randint(0, 120, (256, 256), device="cuda", dtype=torch.uint8)
+sa = torch.randint(120, 130, (256, 8), device="cuda", dtype=torch.uint8)
+for cg in (1, 2):
+    P.gemm_mxfp8(qa.view(torch.float8_e4m3fn), sa, qa.view(torch.float8_e4m3fn), sa, cta_group=cg)
+xl = torch.randn(6, 5000, device="cuda")
+P.layernorm(xl, torch.ones(5000, device="cuda"), torch.zeros(5000, device="cuda"))
+torch.cuda.synchronize()
+print("sanitize run ok")

@@ -570,6 +570,56 @@ def bench_layernorm(args, rank, ws, local):
             "clocks": clocks}
 
 
+SIMP_BH, SIMP_S, SIMP_W1, SIMP_W2 = 16, 8192, 32, 512
+
+
+def bench_simplicial(args, rank, ws, local):
+    """2-simplicial attention forward, bf16 [16, 8192,
+    128], windows w1=32 (K1) and w2=512 (K2), heads split across ranks.
+    Algorithmic FLOP = 4*D per (i, j1, j2) triple (QK'.K2 + P.V2)."""
+    import torch
+    import paper_2605_10905_b200 as P
+    from paper_2605_10905_b200 import shard
+    L = P.lib()
+    pk = peaks()
+    dev = torch.device("cuda", local)
+    r0, r1 = shard.head_shards(SIMP_BH, ws)[rank]
+    bh = max(1, r1 - r0)
+    g = torch.Generator(device=dev).manual_seed(31 + rank)
+    t = [((torch.rand((bh, SIMP_S, 128), device=dev, generator=g) * 2 - 1).bfloat16())
+         for _ in range(5)]
+    o = torch.empty_like(t[0])
+    lse = torch.empty((bh, SIMP_S), device=dev, dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def step():
+        P._check(L.mimw_b200_simplicial_attention_fwd(*(x.data_ptr() for x in t), o.data_ptr(),
+                                                      lse.data_ptr(), bh, SIMP_S, 128, SIMP_W1,
+                                                      SIMP_W2, 128 ** -0.5, sptr))
+
+    steps = max(3, args.steps // 5)
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(step, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    i = np.arange(SIMP_S, dtype=np.float64)
+    triples = float(np.sum(np.minimum(SIMP_W1, i + 1) * np.minimum(SIMP_W2, i + 1)))
+    flop_head = 4.0 * 128 * triples
+    per = secs / steps
+    achieved = flop_head * (r1 - r0) / per / 1e12
+    return {"value": round(flop_head * SIMP_BH * steps / secs / 1e12, 2), "unit": "TFLOPS",
+            "ms_per_step": round(per * 1e3, 4), "scaling": "strong",
+            "config": {"workload": "2-simplicial attention fwd (SURVEY §8f rank 2), bf16 BH=16 "
+                                   "S=8192 D=128, w1=32, w2=512",
+                       "l2": "5 x 32 MiB inputs (K2/V2 windows re-read from L2 per K1 offset)"},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
+                         "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
+                         "peak_source": f"{pk['src']} bf16 burst",
+                         "algorithmic_flop_per_launch": flop_head * (r1 - r0), "traffic": None},
+            "clocks": clocks}
+
+
 def torch_empty_cache():
     import torch
     torch.cuda.empty_cache()
@@ -581,7 +631,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm"])
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm", "simplicial"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -625,6 +675,8 @@ def main():
         res = bench_moe(args, rank, ws, local)
     elif args.workload == "layernorm":
         res = bench_layernorm(args, rank, ws, local)
+    elif args.workload == "simplicial":
+        res = bench_simplicial(args, rank, ws, local)
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
@@ -640,6 +692,7 @@ def main():
                 "reassembly")}
             torch_empty_cache()
             res["secondary"]["layernorm_cluster"] = bench_layernorm(args, rank, ws, local)
+            res["secondary"]["simplicial_attention"] = bench_simplicial(args, rank, ws, local)
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

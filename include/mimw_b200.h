@@ -116,6 +116,27 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
                             int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
                             int64_t window, double scale, void *stream);
 
+/* ---- 2-simplicial attention forward ----------------
+ * Replaces: void oracle_simplicial_attention(q, k1, v1, k2, v2, int w1, int w2,
+ *                                            double scale, Tile *o, Tile *lse)
+ *           proj/core/include/mimw/oracles.hpp:31-33 (oracles.cpp:82-117):
+ *   s(i,j1,j2) = scale * sum_x q[i,x] k1[j1,x] k2[j2,x],
+ *   o[i] = sum softmax(s) v1[j1] (.) v2[j2],  lse[i] = log sum exp s,
+ *   j1 in [i-w1+1, i], j2 in [i-w2+1, i].
+ * Host f32 buffers of [seq, d] (d <= 128, zero-padded to 128 internally). */
+int mimw_b200_oracle_simplicial_attention(const float *q, const float *k1, const float *v1,
+                                           const float *k2, const float *v2, float *o, float *lse,
+                                           int64_t seq, int64_t d, int64_t w1, int64_t w2,
+                                           double scale);
+
+/* Device form: bf16 [bh, seq, 128] contiguous (bh = batch*heads), lse fp32
+ * [bh, seq] or NULL.  Per K1 offset a windowed flash-attention sweep over K2/V2
+ * on tcgen05 (Q (.) K1 formed elementwise into smem, V1 applied after P.V2). */
+int mimw_b200_simplicial_attention_fwd(const void *q, const void *k1, const void *v1, const void *k2,
+                                       const void *v2, void *o, float *lse, int64_t bh, int64_t seq,
+                                       int64_t head_dim, int64_t w1, int64_t w2, double scale,
+                                       void *stream);
+
 /* ---- Cluster LayerNorm ------------------------------
  * Replaces: void oracle_layernorm(const Tile &x, const Tile &w, const Tile &b,
  *                                 double eps, Tile *y, Tile *mean, Tile *rstd)

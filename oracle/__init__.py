@@ -223,6 +223,26 @@ def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: floa
     return o, lse
 
 
+def oracle_simplicial_rows(q, k1, v1, k2, v2, w1: int, w2: int, scale: float, rows):
+    """Selected rows of oracle_simplicial_attention (oracles.cpp:82-117), in
+    float64 numpy (rows are independent, so this is exact oracle semantics for
+    those rows): returns (o[len(rows), D], lse[len(rows)])."""
+    q, k1, v1, k2, v2 = (np.asarray(t, np.float64) for t in (q, k1, v1, k2, v2))
+    out_o, out_l = [], []
+    for i in rows:
+        j1 = np.arange(max(0, i - w1 + 1), i + 1)
+        j2 = np.arange(max(0, i - w2 + 1), i + 1)
+        s = ((q[i] * k1[j1]) @ k2[j2].T) * scale          # [|j1|, |j2|]
+        m = s.max()
+        e = np.exp(s - m)
+        l_ = e.sum()
+        p = e / l_
+        o = (p[:, :, None] * v1[j1][:, None, :] * v2[j2][None, :, :]).sum(axis=(0, 1))
+        out_o.append(o.astype(np.float32))
+        out_l.append(np.float32(m + np.log(l_)))
+    return np.stack(out_o), np.array(out_l, np.float32)
+
+
 def oracle_layernorm(x, w, b, eps: float):
     x, w, b = map(_f32, (x, w, b))
     rows, n = x.shape

@@ -74,6 +74,8 @@ def _optional_sigs():
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
                                                                            C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
+        "mimw_b200_oracle_simplicial_attention": [_fp] * 7 + [_i64] * 4 + [C.c_double],
+        "mimw_b200_simplicial_attention_fwd": [_vp] * 6 + [_vp] + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_oracle_layernorm": [_fp, _fp, _fp, C.c_double, _fp, _fp, _fp, _i64, _i64],
         "mimw_b200_layernorm": [_vp] * 6 + [_i64, _i64, C.c_double, _vp],
         "mimw_b200_layernorm_ex": [_vp] * 6 + [_i64, _i64, C.c_double, C.c_int32, _vp],
@@ -143,6 +145,19 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
     return (o, lse) if with_lse else o
 
 
+def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float):
+    """``oracle_simplicial_attention`` (oracles.hpp:31-33, oracles.cpp:82-117)
+    on the B200 kernel for one [S, D] head; returns (o, lse)."""
+    q, k1, v1, k2, v2 = map(_f32, (q, k1, v1, k2, v2))
+    s, d = q.shape
+    o = np.empty((s, d), np.float32)
+    lse = np.empty(s, np.float32)
+    _check(lib().mimw_b200_oracle_simplicial_attention(_ptr(q), _ptr(k1), _ptr(v1), _ptr(k2),
+                                                       _ptr(v2), _ptr(o), _ptr(lse), s, d, w1, w2,
+                                                       scale))
+    return o, lse
+
+
 def oracle_layernorm(x, w, b, eps: float):
     """``oracle_layernorm(x, w, b, eps, &y, &mean, &rstd)`` (oracles.cpp:28-55)
     on the B200 cluster kernel; returns (y, mean, rstd)."""
@@ -165,6 +180,11 @@ def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: 
     if name == "multi_device_gemm":
         return {"c": oracle_multi_device_gemm(inputs["a0"], inputs["a1"], inputs["b0"],
                                               inputs["b1"], precision)}
+    if name == "simplicial_attention":
+        o, lse = oracle_simplicial_attention(inputs["q"], inputs["k1"], inputs["v1"], inputs["k2"],
+                                             inputs["v2"], int(scalars["w1"]), int(scalars["w2"]),
+                                             scalars["scale"])
+        return {"o": o, "lse": lse}
     if name == "layernorm":
         return {"y": oracle_layernorm(inputs["x"], inputs["w"], inputs["b"],
                                       scalars.get("eps", 1e-5))[0]}
@@ -281,3 +301,25 @@ def layernorm(x, w, b, eps: float = 1e-5, out=None, mean=None, rstd=None, stream
                                         rstd.data_ptr() if rstd is not None else None, rows, n,
                                         eps, cluster, _stream(stream)))
     return out
+
+
+def simplicial_attention_fwd(q, k1, v1, k2, v2, w1: int, w2: int, scale: float | None = None,
+                             out=None, lse=None, want_lse: bool = True, stream=None):
+    """2-simplicial attention forward on bf16 CUDA tensors [BH, S, 128]."""
+    import torch
+    bh, s, d = q.shape
+    if d != 128:
+        raise MimwError(ERR_UNSUPPORTED, "device simplicial attention supports head_dim == 128")
+    for t in (q, k1, v1, k2, v2):
+        if not t.is_contiguous() or t.shape != q.shape:
+            raise MimwError(ERR_UNSUPPORTED, "contiguous [BH, S, 128] tensors of one shape required")
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None and want_lse:
+        lse = torch.empty((bh, s), device=q.device, dtype=torch.float32)
+    if scale is None:
+        scale = d ** -0.5
+    _check(lib().mimw_b200_simplicial_attention_fwd(
+        q.data_ptr(), k1.data_ptr(), v1.data_ptr(), k2.data_ptr(), v2.data_ptr(), out.data_ptr(),
+        lse.data_ptr() if lse is not None else None, bh, s, d, w1, w2, scale, _stream(stream)))
+    return out, lse

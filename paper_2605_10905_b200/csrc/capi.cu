@@ -20,6 +20,7 @@
 #include "gemm_bf16.h"
 #include "gemm_mxfp8.h"
 #include "layernorm_cluster.h"
+#include "simplicial_fwd.h"
 
 namespace {
 
@@ -331,6 +332,43 @@ void layernorm_checks(const void *x, const void *w, const void *b, const void *y
   require(x && w && b && y, MIMW_ERR_ARG, "null pointer");
 }
 
+// oracle_simplicial_attention (oracles.cpp:82-117) for one [seq, d] head of
+// host f32 Tiles; d <= 128 zero-padded to 128 (exact, as host_attention).
+void host_simplicial(const float *q, const float *k1, const float *v1, const float *k2,
+                     const float *v2, float *o, float *lse, int64_t seq, int64_t d, int64_t w1,
+                     int64_t w2, double scale) {
+  require(seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
+  require((w1 >= 1 && w2 >= 1) || seq == 0, MIMW_ERR_ARG, "windows must be >= 1");
+  if (seq == 0) return;
+  require(q && k1 && v1 && k2 && v2 && o, MIMW_ERR_ARG, "null pointer");
+  require_sm100();
+  cudaStream_t s = cudaStreamPerThread;
+  const int64_t n = seq * d;
+  DevBuf din(sizeof(float) * 5 * n, s);
+  DevBuf dx(2 * 5 * seq * 128, s), dout(2 * seq * 128, s), dlse(sizeof(float) * seq, s),
+      dof(sizeof(float) * (n ? n : 1), s);
+  const float *src[5] = {q, k1, v1, k2, v2};
+  void *dst[5];
+  for (int t = 0; t < 5; ++t) {
+    float *f = din.as<float>() + t * n;
+    dst[t] = static_cast<char *>(dx.p) + (size_t)t * seq * 128 * 2;
+    if (n) check_cuda(cudaMemcpyAsync(f, src[t], sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D");
+    mimw::stage_cols_bf16(f, seq, d, 128, dst[t], 128, 0, 0, s);
+  }
+  check_cuda(cudaGetLastError(), "staging kernels");
+  mimw::SimplicialArgs a{dst[0], dst[1], dst[2], dst[3], dst[4], dout.p, dlse.as<float>(),
+                         1, seq, w1, w2, scale};
+  check_cuda(mimw::simplicial_fwd_launch(a, s), "simplicial launch");
+  if (n) {
+    mimw::unpad_bf16_to_f32(dout.p, 128, dof.as<float>(), seq, d, s);
+    check_cuda(cudaGetLastError(), "unpad");
+    check_cuda(cudaMemcpyAsync(o, dof.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H o");
+  }
+  if (lse) check_cuda(cudaMemcpyAsync(lse, dlse.p, sizeof(float) * seq, cudaMemcpyDeviceToHost, s), "D2H lse");
+  check_cuda(cudaStreamSynchronize(s), "simplicial execution");
+}
+
 }  // namespace
 
 extern "C" {
@@ -481,6 +519,32 @@ int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const v
   return guarded([&] {
     grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, true,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mimw_b200_oracle_simplicial_attention(const float *q, const float *k1, const float *v1,
+                                           const float *k2, const float *v2, float *o, float *lse,
+                                           int64_t seq, int64_t d, int64_t w1, int64_t w2,
+                                           double scale) {
+  return guarded([&] { host_simplicial(q, k1, v1, k2, v2, o, lse, seq, d, w1, w2, scale); });
+}
+
+int mimw_b200_simplicial_attention_fwd(const void *q, const void *k1, const void *v1, const void *k2,
+                                       const void *v2, void *o, float *lse, int64_t bh, int64_t seq,
+                                       int64_t head_dim, int64_t w1, int64_t w2, double scale,
+                                       void *stream) {
+  return guarded([&] {
+    require(bh >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
+    require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device simplicial attention supports head_dim == 128");
+    require(w1 >= 1 && w2 >= 1, MIMW_ERR_ARG, "windows must be >= 1");
+    require(seq < (1ll << 31) && bh * ((seq + 127) / 128) < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent too large");
+    if (bh == 0 || seq == 0) return;
+    require(q && k1 && v1 && k2 && v2 && o, MIMW_ERR_ARG, "null pointer");
+    require((((uintptr_t)q | (uintptr_t)k1 | (uintptr_t)v1 | (uintptr_t)k2 | (uintptr_t)v2 | (uintptr_t)o) & 15) == 0,
+            MIMW_ERR_UNSUPPORTED, "tensors must be 16-byte aligned");
+    require_sm100();
+    mimw::SimplicialArgs a{q, k1, v1, k2, v2, o, lse, bh, seq, w1, w2, scale};
+    check_cuda(mimw::simplicial_fwd_launch(a, static_cast<cudaStream_t>(stream)), "simplicial launch");
   });
 }
 

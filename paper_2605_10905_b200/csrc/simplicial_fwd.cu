@@ -1,0 +1,428 @@
+// 2-simplicial (trilinear) attention forward for sm_100a:
+//
+//   s(i, j1, j2) = scale * sum_x q[i,x] k1[j1,x] k2[j2,x]
+//   o[i,x]       = sum_{j1,j2} softmax_{(j1,j2)}(s) v1[j1,x] v2[j2,x]
+//   lse[i]       = log sum exp s
+//   j1 in [max(0, i-w1+1), i],  j2 in [max(0, i-w2+1), i]
+//
+// i.e. oracle_simplicial_attention (proj/core/src/oracles.cpp:82-117), the
+// computation of proj/kernels/simplicial_attention.mimw:1-95.  The tensor-core
+// form the paper describes (form Q (.) K1 elementwise, GEMM
+// against K2, online softmax, P.V2 GEMM, apply V1 after) maps to B200 as a
+// loop over the K1 offset d = i - j1 (0 <= d < w1), each d a windowed
+// flash-attention sweep over K2/V2 tiles:
+//   Q'_d[i]  = q[i] (.) k1[i - d]             (softmax warps -> smem, SW128)
+//   S        = Q'_d K2_t^T                    (tcgen05.mma SS -> TMEM)
+//   U_d     += P V2_t                          (tcgen05.mma TS, P in TMEM)
+//   O[i]    += v1[i - d] (.) U_d[i]           (softmax warps, TMEM -> TMEM)
+// with ONE running max / sum per row across all (d, j2), so O and U are
+// rescaled together (only when the max grows by > 8 in log2 units).
+//
+// MIMW roles (one CTA = 128 query rows of one (batch, head), 6 warps):
+//   warp 0     TMA producer of the K2/V2 tile ring (repeated for every d)
+//   warp 1     TMEM allocator + single-thread MMA issuer; S(step n) is issued
+//              before PV(step n-1) so the next S overlaps the softmax
+//   warps 2-5  Q' preparation, softmax, U -> O fold, epilogue (1 row/thread)
+// TMEM: S [0,128) f32, P [128,192) bf16, U [256,384) f32, O [384,512) f32.
+#include "simplicial_fwd.h"
+#include "ptx.cuh"
+#include "tma_host.h"
+
+#include <algorithm>
+
+namespace mimw {
+
+namespace {
+
+constexpr int D = 128;
+constexpr int BQ = 128;
+constexpr int BKV = 128;
+constexpr int NSLOT = 4;
+constexpr int TILE_BYTES = BKV * D * 2;     // 32 KiB
+constexpr int HALF_BYTES = TILE_BYTES / 2;  // one 64-column swizzle panel
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_QP = 0;                               // 2 Q' buffers
+constexpr int SMEM_KV = 2 * TILE_BYTES;                  // K2/V2 ring
+constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
+constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
+constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);
+constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_U = 256, TM_O = 384;
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct Params {
+  const __nv_bfloat16 *q, *k1, *v1;  // [bh, seq, 128]
+  __nv_bfloat16 *o;
+  float *lse;
+  int seq, w1, w2, nqt;
+  float scale_log2;
+};
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// K2/V2 tile range [lo, hi] needed by query rows [i0, i0+127]
+__device__ __forceinline__ void kv2_range(int i0, const Params &p, int &lo, int &hi) {
+  lo = max(0, i0 - p.w2 + 1) / BKV;
+  hi = min(i0 + BQ - 1, p.seq - 1) / BKV;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
+                      Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bars = sbase + SMEM_BAR;
+  auto qp_full = [&](int b) { return bars + 8 * b; };
+  auto qp_empty = [&](int b) { return bars + 16 + 8 * b; };
+  const uint32_t s_full = bars + 32, s_free = bars + 40, p_full = bars + 48, u_done = bars + 56;
+  auto kv_full = [&](int s) { return bars + 64 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 64 + 8 * NSLOT + 8 * s; };
+  const uint32_t tmem_slot = bars + 64 + 16 * NSLOT;
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 64 + 16 * NSLOT);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = lane_id();
+  const int bh = blockIdx.x / p.nqt;
+  const int qt = p.nqt - 1 - (int)(blockIdx.x % p.nqt);  // heavier (later) tiles first
+  const int i0 = qt * BQ;
+  int lo, hi;
+  kv2_range(i0, p, lo, hi);
+  const int ntile = hi - lo + 1;
+  const int nd = min(p.w1, i0 + BQ);  // K1 offsets d with at least one valid row
+  const int nsteps = nd * ntile;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmK2);
+    tma_prefetch_desc(&tmV2);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(qp_full(b), 4);
+      mbar_init(qp_empty(b), 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(u_done, 1);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(kv_full(s), 1);
+      mbar_init(kv_empty(s), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ================= TMA producer: K2_t, V2_t for every (d, t) =================
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int n = 0; n < nsteps; ++n) {
+        const int t = lo + n % ntile;
+#pragma unroll 1
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(kv_empty(slot), ph ^ 1, 70);
+          mbar_arrive_expect_tx(kv_full(slot), TILE_BYTES);
+          const uint32_t dst = sbase + SMEM_KV + slot * TILE_BYTES;
+          const CUtensorMap *tm = kv == 0 ? &tmK2 : &tmV2;
+          tma_load_3d(dst, tm, kv_full(slot), 0, t * BKV, bh);
+          tma_load_3d(dst + HALF_BYTES, tm, kv_full(slot), 64, t * BKV, bh);
+          if (++slot == NSLOT) { slot = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);
+    constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;
+    constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;
+    uint32_t sf_phase = 0, pf_phase = 0;
+    auto ring_wait = [&](int pos) { mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71); };
+    auto issue_S = [&](int n) {  // S of step n = (d, t)
+      const int d = n / ntile;
+      const int t = n % ntile;
+      if (t == 0) mbar_wait(qp_full(d & 1), (d >> 1) & 1, 72);
+      ring_wait(2 * n);
+      mbar_wait(s_free, sf_phase ^ 1, 73);
+      sf_phase ^= 1;
+      tc_fence_after();
+      const uint32_t qa = (sbase + SMEM_QP + (d & 1) * TILE_BYTES) >> 4;
+      const uint32_t kb = (sbase + SMEM_KV + ((2 * n) % NSLOT) * TILE_BYTES) >> 4;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = ((k >> 2) * HALF_BYTES + (k & 3) * 32) >> 4;
+          mma_f16_ss<1>(tmem + TM_S, make_desc(LO_KMAJ | (qa + off), HI_KMAJ),
+                        make_desc(LO_KMAJ | (kb + off), HI_KMAJ), IDESC_S, k != 0);
+        }
+        mma_commit(s_full);
+        mma_commit(kv_empty((2 * n) % NSLOT));
+        if (t == ntile - 1) mma_commit(qp_empty(d & 1));  // last read of Q'_d
+      }
+      __syncwarp();
+    };
+    auto issue_PV = [&](int n) {
+      const int t = n % ntile;
+      ring_wait(2 * n + 1);
+      mbar_wait(p_full, pf_phase, 74);
+      pf_phase ^= 1;
+      tc_fence_after();
+      const uint32_t vb = (sbase + SMEM_KV + ((2 * n + 1) % NSLOT) * TILE_BYTES) >> 4;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          mma_f16_ts<1>(tmem + TM_U, tmem + TM_P + k * 8,
+                        make_desc(LO_VMN | (vb + k * (2048 >> 4)), HI_KMAJ), IDESC_PV,
+                        (t != 0 || k != 0) ? 1u : 0u);
+        mma_commit(u_done);
+        mma_commit(kv_empty((2 * n + 1) % NSLOT));
+      }
+      __syncwarp();
+    };
+    for (int n = 0; n <= nsteps; ++n) {
+      if (n < nsteps) issue_S(n);
+      if (n > 0) issue_PV(n - 1);
+    }
+  } else {
+    // ================= Q' prep / softmax / U->O fold / epilogue =================
+    const int q = warp & 3;
+    const int row = q * 32 + (int)lane;  // row of the tile == TMEM lane
+    const int i = i0 + row;
+    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+    const bool row_live = i < p.seq;
+    const __nv_bfloat16 *qrow = p.q + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D;
+    float m_used = -INFINITY, l = 0.f;
+    uint32_t s_phase = 0;
+    int pv_seen = 0;  // PV steps known complete (u_done phases consumed)
+    auto wait_pv = [&](int k) {  // PV of step k complete
+      while (pv_seen <= k) {
+        mbar_wait(u_done, (uint32_t)(pv_seen & 1), 77);
+        ++pv_seen;
+      }
+      tc_fence_after();
+    };
+    bool o_live = false;  // O holds a folded U
+    // ---- Q'_d = q (.) k1[i - d] into smem buffer d&1 (SW128 K-major) ----
+    auto prep_qp = [&](int d) {
+      const int j1 = i - d;
+      if (d >= 2) mbar_wait(qp_empty(d & 1), ((d >> 1) & 1) ^ 1, 75);
+      const uint32_t buf = sbase + SMEM_QP + (d & 1) * TILE_BYTES;
+      const bool ok = row_live && j1 >= 0;
+      const uint4 *qv = reinterpret_cast<const uint4 *>(qrow);
+      const uint4 *kv = reinterpret_cast<const uint4 *>(p.k1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
+#pragma unroll 4
+      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 bf16
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (ok) {
+          const uint4 a = __ldg(qv + c), b = __ldg(kv + c);
+          const uint32_t *pa = &a.x, *pb = &b.x;
+          uint32_t *pw = &w.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pa + e));
+            const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pb + e));
+            pw[e] = pack_bf16(fa.x * fb.x, fa.y * fb.y);
+          }
+        }
+        const int panel = c >> 3, cc = c & 7;
+        st_shared_v4(buf + panel * HALF_BYTES + (row >> 3) * 1024 + (row & 7) * 128 +
+                         ((cc ^ (row & 7)) << 4),
+                     w.x, w.y, w.z, w.w);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qp_full(d & 1));
+    };
+    const float sl = p.scale_log2;
+    for (int n = 0; n < nsteps; ++n) {
+      const int d = n / ntile;
+      const int t = n % ntile;
+      const int j1 = i - d;
+      if (n == 0) prep_qp(0);
+      // ---- S of step n ----
+      mbar_wait(s_full, s_phase, 76);
+      s_phase ^= 1;
+      tc_fence_after();
+      uint32_t s[128];
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);
+      // mask: j2 in [i - w2 + 1, i], valid query row, valid K1 row
+      const int k0 = (lo + t) * BKV;
+      const int c_lo = i - p.w2 + 1 - k0;
+      const int c_hi = min(i, p.seq - 1) - k0;
+      const bool live = row_live && j1 >= 0;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        float v = __uint_as_float(s[c]) * sl;
+        if (!live || c < c_lo || c > c_hi) v = -INFINITY;
+        s[c] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      float corr = 1.f;
+      bool rescale = false;
+      if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
+        corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
+        rescale = m_used != -INFINITY;
+        m_used = mx;
+      }
+      l *= corr;
+      const float nm = (m_used == -INFINITY) ? 0.f : m_used;
+      uint32_t pk[64];
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const float p0 = ex2(__uint_as_float(s[2 * e]) - nm);
+        const float p1 = ex2(__uint_as_float(s[2 * e + 1]) - nm);
+        acc += p0 + p1;
+        pk[e] = pack_bf16(p0, p1);
+      }
+      l += acc;
+      // PV of the previous step must be done before P / U / O are touched
+      if (n > 0) wait_pv(n - 1);
+      if (__any_sync(0xffffffffu, rescale)) {
+        // U (this d's partial sum, if any PV of it ran) and O carry the old max
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t o[32];
+          if (t > 0) {
+            tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x16(tmem + t_lane + TM_U + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
+            tmem_st_32x32b_x16(tmem + t_lane + TM_U + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
+          }
+          if (o_live) {
+            tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x16(tmem + t_lane + TM_O + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
+            tmem_st_32x32b_x16(tmem + t_lane + TM_O + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 64; c += 16)
+        tmem_st_32x32b_x16(tmem + t_lane + TM_P + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (t == ntile - 1) {
+        // next d's Q' first: its S may enter the pipe while this d is folded
+        if (d + 1 < nd) prep_qp(d + 1);
+        // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
+        wait_pv(n);
+        const uint4 *vv = reinterpret_cast<const uint4 *>(p.v1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t u[32], o[32];
+          tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, u);
+          if (o_live) tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint4 w = make_uint4(0, 0, 0, 0);
+            if (live) w = __ldg(vv + c / 8 + g);
+            const uint32_t *pw = &w.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pw + e));
+              const int x = g * 8 + e * 2;
+              const float b0 = o_live ? __uint_as_float(o[x]) : 0.f;
+              const float b1 = o_live ? __uint_as_float(o[x + 1]) : 0.f;
+              o[x] = __float_as_uint(b0 + f.x * __uint_as_float(u[x]));
+              o[x + 1] = __float_as_uint(b1 + f.y * __uint_as_float(u[x + 1]));
+            }
+          }
+          tmem_st_32x32b_x16(tmem + t_lane + TM_O + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
+          tmem_st_32x32b_x16(tmem + t_lane + TM_O + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
+        }
+        tmem_st_wait();
+        o_live = true;
+        // the PV issuer overwrites U with the next d's first PV only after the
+        // next P arrives, which this warp publishes after these loads
+        tc_fence_before();
+      }
+    }
+    // ---------------- epilogue: O / l, lse ----------------
+    const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+    if (row_live && p.lse != nullptr)
+      p.lse[(size_t)bh * p.seq + i] = (m_used + __log2f(l)) * (1.0f / LOG2E);
+    uint4 *orow = reinterpret_cast<uint4 *>(p.o + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D);
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
+      tmem_ld_wait();
+      if (row_live) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l);
+          w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l);
+          w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l);
+          w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l);
+          orow[c / 8 + v] = w;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 512);
+  }
+}
+
+}  // namespace
+
+cudaError_t simplicial_fwd_launch(const SimplicialArgs &a, cudaStream_t stream) {
+  const uint64_t bh = (uint64_t)a.bh;
+  if (bh == 0 || a.seq == 0) return cudaSuccess;
+  CUtensorMap tK2 = make_tmap_3d(a.k2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tV2 = make_tmap_3d(a.v2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  Params p;
+  p.q = static_cast<const __nv_bfloat16 *>(a.q);
+  p.k1 = static_cast<const __nv_bfloat16 *>(a.k1);
+  p.v1 = static_cast<const __nv_bfloat16 *>(a.v1);
+  p.o = static_cast<__nv_bfloat16 *>(a.o);
+  p.lse = a.lse;
+  p.seq = (int)a.seq;
+  p.w1 = (int)std::min<int64_t>(a.w1, a.seq);
+  p.w2 = (int)std::min<int64_t>(a.w2, a.seq);
+  p.nqt = (int)((a.seq + BQ - 1) / BQ);
+  p.scale_log2 = (float)(a.scale * 1.4426950408889634);
+  cudaError_t e = cudaFuncSetAttribute(simplicial_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
+  simplicial_fwd_kernel<<<(unsigned)(bh * p.nqt), NUM_THREADS, SMEM_TOTAL, stream>>>(tK2, tV2, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mimw

@@ -97,6 +97,62 @@ int mimw_b200_oracle_multi_device_gemm(const float *a0, const float *a1, const f
                                        const float *b1, float *c, int64_t m, int64_t k0,
                                        int64_t k1, int64_t n, int32_t precision);
 
+/* ---- All-gather (K-gathered) multi-device GEMM -------
+ * The production form of oracle_multi_device_gemm (oracles.hpp:24-25,
+ * oracles.cpp:57-80) and proj/kernels/multi_device_gemm.mimw:1-79,
+ * generalised from 2 to `world` devices.  Device s holds the K-split
+ * a_splits[s] bf16 [m, k_splits[s]] and b_splits[s] bf16 [k_splits[s], n];
+ * this call (on device `rank`) computes its row block of
+ *     C = [a_0 | ... | a_{world-1}] . [b_0 ; ... ; b_{world-1}]
+ * i.e. c[rows, n] (bf16, row pitch ldc) = C[row0 : row0 + rows, :].
+ * a_splits[s] / b_splits[s] are pointers valid in the calling process: the
+ * local split, or a peer's buffer mapped with mimw_b200_ipc_open.  One kernel
+ * overlaps the gather with the GEMM: comm CTA pairs pull the peers' splits
+ * over NVLink into `workspace` in 256-wide K slabs and publish each on a
+ * readiness counter; the GEMM CTA pairs start on the local split and wait on a
+ * slab's counter only before its first TMA load.
+ * pads[p] = device p's 64-byte signal pad (inside an IPC allocation, zeroed at
+ * allocation) for the device-side entry/exit barrier, with `epoch` strictly
+ * increasing from 1 per call; pads == NULL skips the barrier (the caller then
+ * guarantees the peers' splits are complete and stay unchanged until this call
+ * has finished — e.g. all "devices" emulated on one GPU).
+ * workspace: >= mimw_b200_multi_device_gemm_workspace_bytes(...), 1 KiB
+ * aligned.  n and every k split multiples of 8.  comm_pairs: > 0 that many
+ * dedicated comm CTA pairs (the reference's comm CTAs); < 0 a comm warp in
+ * every GEMM CTA pair instead (no SM taken from the GEMM); 0 = the default.
+ * max_pairs caps the GEMM CTA pairs (0 = every co-resident pair). */
+#define MIMW_MAX_DEVICES 8
+#define MIMW_IPC_HANDLE_BYTES 64
+#define MIMW_SIGNAL_PAD_BYTES 64
+int64_t mimw_b200_multi_device_gemm_workspace_bytes(int32_t rank, int32_t world,
+                                                    const int64_t *k_splits, int64_t rows,
+                                                    int64_t n);
+int mimw_b200_multi_device_gemm(int32_t rank, int32_t world, const void *const *a_splits,
+                                const void *const *b_splits, const int64_t *k_splits, int64_t m,
+                                int64_t n, int64_t row0, int64_t rows, void *c, int64_t ldc,
+                                void *workspace, int64_t workspace_bytes, uint32_t *const *pads,
+                                uint32_t epoch, int32_t comm_pairs, int32_t max_pairs,
+                                void *stream);
+
+/* Same, with the comm pipelines' tuning knobs (0 = defaults): comm_box = box
+ * rows 32 / 64 / 128 of 512 bytes (16 / 32 / 64 KiB TMA boxes), comm_agents = copy
+ * pipelines per comm CTA (1..6), comm_lag = stores in flight before a slab's
+ * readiness signal waits for completion (1, 2, 4, 6, 8, 12). */
+int mimw_b200_multi_device_gemm_ex(int32_t rank, int32_t world, const void *const *a_splits,
+                                   const void *const *b_splits, const int64_t *k_splits, int64_t m,
+                                   int64_t n, int64_t row0, int64_t rows, void *c, int64_t ldc,
+                                   void *workspace, int64_t workspace_bytes, uint32_t *const *pads,
+                                   uint32_t epoch, int32_t comm_pairs, int32_t max_pairs,
+                                   int32_t comm_box, int32_t comm_agents, int32_t comm_lag,
+                                   void *stream);
+
+/* CUDA IPC plumbing for the peer mappings: a zero-filled device allocation
+ * with its 64-byte IPC handle, and the peer side's open / close. */
+int mimw_b200_ipc_alloc(int64_t bytes, void **ptr, void *handle);
+int mimw_b200_ipc_open(const void *handle, void **ptr);
+int mimw_b200_ipc_close(void *ptr);
+int mimw_b200_ipc_free(void *ptr);
+
 /* ---- Attention forward (windowed causal softmax attention) --------------
  * Replaces: void oracle_attention(const Tile &q, const Tile &k, const Tile &v,
  *                                 int w, double scale, Tile *o)

@@ -678,4 +678,124 @@ int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int
   });
 }
 
+// ---- all-gather multi-device GEMM ------------------------
+int64_t mimw_b200_multi_device_gemm_workspace_bytes(int32_t rank, int32_t world,
+                                                    const int64_t *k_splits, int64_t rows,
+                                                    int64_t n) {
+  if (world < 1 || world > MIMW_MAX_DEVICES || rank < 0 || rank >= world || !k_splits || rows < 0 ||
+      n < 0)
+    return -1;
+  return (int64_t)mimw::multi_device_gemm_workspace_bytes(rank, world, k_splits, rows, n);
+}
+
+int mimw_b200_multi_device_gemm_ex(int32_t rank, int32_t world, const void *const *a_splits,
+                                   const void *const *b_splits, const int64_t *k_splits, int64_t m,
+                                   int64_t n, int64_t row0, int64_t rows, void *c, int64_t ldc,
+                                   void *workspace, int64_t workspace_bytes, uint32_t *const *pads,
+                                   uint32_t epoch, int32_t comm_pairs, int32_t max_pairs,
+                                   int32_t comm_box, int32_t comm_agents, int32_t comm_lag,
+                                   void *stream) {
+  return guarded([&] {
+    require(world >= 1 && world <= MIMW_MAX_DEVICES && rank >= 0 && rank < world, MIMW_ERR_ARG,
+            "rank/world out of range (world <= MIMW_MAX_DEVICES)");
+    require(a_splits && b_splits && k_splits, MIMW_ERR_ARG, "null split arrays");
+    require(m >= 0 && n >= 0 && row0 >= 0 && rows >= 0 && row0 + rows <= m, MIMW_ERR_SHAPE,
+            "row range [row0, row0 + rows) outside [0, m)");
+    require(n % 8 == 0, MIMW_ERR_UNSUPPORTED, "n must be a multiple of 8 (16-byte TMA rows)");
+    mimw::MultiDeviceGemmArgs g{};
+    g.rank = rank;
+    g.world = world;
+    bool any_pad = false, all_pad = true;
+    for (int s = 0; s < world; ++s) {
+      require(k_splits[s] >= 0, MIMW_ERR_SHAPE, "negative K split");
+      require(k_splits[s] % 8 == 0, MIMW_ERR_UNSUPPORTED,
+              "every K split must be a multiple of 8 (16-byte TMA rows)");
+      if (k_splits[s] && rows && n) {
+        require(a_splits[s] && b_splits[s], MIMW_ERR_ARG, "null split pointer");
+        require_pitch(a_splits[s], k_splits[s], 2, "a split");
+        require_pitch(b_splits[s], n, 2, "b split");
+      }
+      g.a[s] = a_splits[s];
+      g.b[s] = b_splits[s];
+      g.k[s] = k_splits[s];
+      const bool has = pads && pads[s];
+      any_pad |= has;
+      all_pad &= has;
+      g.pads[s] = has ? pads[s] : nullptr;
+    }
+    require(!any_pad || all_pad, MIMW_ERR_ARG, "pads: give every device's signal pad or none");
+    require(!any_pad || epoch != 0, MIMW_ERR_ARG, "epoch must be >= 1 with a device barrier");
+    const bool work = rows > 0 && n > 0;
+    if (!work && !any_pad) return;  // nothing to compute, no peers to meet
+    require(workspace != nullptr, MIMW_ERR_ARG, "null workspace");
+    if (work) {
+      require(c != nullptr, MIMW_ERR_ARG, "null output");
+      require_pitch(c, ldc, 2, "c");
+    }
+    require(((uintptr_t)workspace & 1023) == 0, MIMW_ERR_UNSUPPORTED, "workspace not 1 KiB aligned");
+    const int64_t need = (int64_t)mimw::multi_device_gemm_workspace_bytes(rank, world, k_splits, rows, n);
+    require(workspace_bytes >= need, MIMW_ERR_ARG,
+            "workspace too small: need " + std::to_string(need) + " bytes");
+    require_sm100();
+    g.n = n;
+    g.row0 = row0;
+    g.rows = rows;
+    g.c = c;
+    g.ldc = ldc;
+    g.ws = workspace;
+    g.ws_bytes = (size_t)workspace_bytes;
+    g.epoch = epoch;
+    g.comm_clusters = comm_pairs;  // 0 default, > 0 dedicated comm pairs, < 0 distributed comm warps
+    g.max_clusters = max_pairs;
+    g.comm_box = comm_box;
+    g.comm_agents = comm_agents;
+    g.comm_lag = comm_lag;
+    check_cuda(mimw::multi_device_gemm_launch(g, static_cast<cudaStream_t>(stream)),
+               "multi-device gemm launch");
+  });
+}
+
+int mimw_b200_multi_device_gemm(int32_t rank, int32_t world, const void *const *a_splits,
+                                const void *const *b_splits, const int64_t *k_splits, int64_t m,
+                                int64_t n, int64_t row0, int64_t rows, void *c, int64_t ldc,
+                                void *workspace, int64_t workspace_bytes, uint32_t *const *pads,
+                                uint32_t epoch, int32_t comm_pairs, int32_t max_pairs,
+                                void *stream) {
+  return mimw_b200_multi_device_gemm_ex(rank, world, a_splits, b_splits, k_splits, m, n, row0, rows,
+                                        c, ldc, workspace, workspace_bytes, pads, epoch, comm_pairs,
+                                        max_pairs, 0, 0, 0, stream);
+}
+
+// ---- CUDA IPC plumbing for the peer mappings ----------------------------------
+int mimw_b200_ipc_alloc(int64_t bytes, void **ptr, void *handle) {
+  return guarded([&] {
+    require(bytes > 0 && ptr && handle, MIMW_ERR_ARG, "bad ipc_alloc arguments");
+    require_sm100();
+    check_cuda(cudaMalloc(ptr, (size_t)bytes), "cudaMalloc");
+    check_cuda(cudaMemset(*ptr, 0, (size_t)bytes), "cudaMemset");
+    cudaIpcMemHandle_t h;
+    check_cuda(cudaIpcGetMemHandle(&h, *ptr), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == MIMW_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int mimw_b200_ipc_open(const void *handle, void **ptr) {
+  return guarded([&] {
+    require(handle && ptr, MIMW_ERR_ARG, "bad ipc_open arguments");
+    require_sm100();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    check_cuda(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int mimw_b200_ipc_close(void *ptr) {
+  return guarded([&] { check_cuda(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); });
+}
+
+int mimw_b200_ipc_free(void *ptr) {
+  return guarded([&] { check_cuda(cudaFree(ptr), "cudaFree"); });
+}
+
 }  // extern "C"

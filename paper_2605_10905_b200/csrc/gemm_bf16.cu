@@ -32,6 +32,7 @@
 #include "tma_host.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace mimw {
@@ -47,7 +48,7 @@ constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int ACC_STAGES = 2;    // TMEM accumulators (2 x 256 columns = 512)
 constexpr int EPI_COLS = 32;     // columns per epilogue store chunk
 
-template <int CG, bool B_MN, typename OutT>
+template <int CG, bool B_MN, typename OutT, bool GATHER = false>
 struct Cfg {
   static constexpr int NB_CTA = BN / CG;                       // B columns staged per CTA
   static constexpr int A_BYTES = BM_CTA * BK * 2;              // 16 KiB
@@ -56,8 +57,11 @@ struct Cfg {
   static constexpr int STAGES = (CG == 2) ? 6 : 4;
   static constexpr int EPI_BUF = 32 * EPI_COLS * (int)sizeof(OutT);   // per warp per buffer
   static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES + EPI_BYTES;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;            // + barriers + align slack
+  static constexpr int COMM_EXTRA = GATHER ? 16384 : 0;        // distributed comm warp's buffer
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES + EPI_BYTES + COMM_EXTRA;
+  static constexpr int BAR_BYTES = 256;                        // pipeline barriers + TMEM slot
+  static constexpr int COMM_BAR_BYTES = 8 * 24 + 32;           // all-gather comm barriers + mailboxes
+  static constexpr int SMEM = BAR_OFF + BAR_BYTES + COMM_BAR_BYTES + 1024;  // + align slack
   static constexpr uint32_t IDESC = idesc_bf16(BM_CTA * CG, BN, 0, B_MN ? 1 : 0);
 };
 
@@ -75,6 +79,7 @@ struct TileCoord {
 template <int PAIRS>
 struct SchedT {
   static constexpr bool kGrouped = false;
+  static constexpr bool kGather = false;
   static constexpr int kPairs = PAIRS;  // CTA pairs per cluster sharing each B tile (multicast)
   int num_m, num_n, group, M;           // num_m in cluster tiles (PAIRS M-tiles each)
   __device__ __forceinline__ int num_tiles() const { return num_m * num_n; }
@@ -107,6 +112,7 @@ using Sched = SchedT<1>;
 constexpr int MAX_GROUPS = 128;
 struct GroupedSched {
   static constexpr bool kGrouped = true;
+  static constexpr bool kGather = false;
   static constexpr int kPairs = 1;
   CUtensorMap y[MAX_GROUPS];
   int tile_off[MAX_GROUPS + 1];  // prefix sum of m_tiles(e) * num_n
@@ -138,12 +144,295 @@ struct GroupedSched {
   __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *, int e) const { return &y[e]; }
 };
 
+
+// K-gathered multi-device GEMM (proj/kernels/multi_device_gemm.mimw:1-79,
+// oracle_multi_device_gemm oracles.cpp:57-80, generalised from 2 to `world`
+// K-splits): device s holds A_s [M, k_s] and B_s [k_s, N]; this rank owns
+// C rows [row0, row0 + rows) = sum_s A_s[rows] . B_s.  The kernel runs two
+// kinds of CTA pairs:
+//   comm pairs (the reference's rank-0 "comm" CTA)  pull every remote split
+//     in 256-column K slabs, box by box, from the peer's HBM (NVLink via the
+//     IPC-mapped pointer) through a 6 x 32 KiB smem ring into a local landing
+//     buffer (TMA load -> TMA store), and publish each slab on a readiness
+//     counter (red.release.gpu; the "remote barrier_arrive" of :67);
+//   GEMM pairs (the reference's compute CTA)  run the persistent 2-CTA GEMM
+//     over the splits in rotation order q = 0 (local split, no wait), 1, ...;
+//     the producer waits on a slab's counter (ld.acquire) before its first TMA
+//     load from the landing buffer, so the transfer of split q overlaps the
+//     tensor-core work on splits < q tile by tile.
+constexpr int MAX_SPLITS = 8;
+constexpr int kDefaultCommPairs = -1;  // distributed comm warps (see multi_device_gemm_launch)
+constexpr int COMM_SLAB = 256;   // K columns per readiness counter
+// comm boxes are {256, R} with 512-byte rows (TMA moves long rows far faster
+// than 128-byte ones): A box = one slab's 256 K columns x R rows, B box = 256
+// N columns x R K rows.  R = box rows (32 / 64 / 128: 16 / 32 / 64 KiB).
+constexpr int COMM_W = 256;
+constexpr int COMM_MAX_BUFS = 24;
+constexpr int COMM_SIG = 16;     // ring of pending slab signals per agent (lag < COMM_SIG)
+struct GatherSched : SchedT<1> {
+  static constexpr bool kGather = true;
+  CUtensorMap ga[MAX_SPLITS], gb[MAX_SPLITS];          // GEMM operands, rotation order (q = 0 local)
+  CUtensorMap src_a[MAX_SPLITS], dst_a[MAX_SPLITS];    // comm: peer A rows -> landing (q >= 1)
+  CUtensorMap src_b[MAX_SPLITS], dst_b[MAX_SPLITS];    // comm: peer B -> landing (q >= 1)
+  int ks[MAX_SPLITS];
+  int nsplit, kblocks, comm_clusters, max_slabs, rbox, nbox;
+  int box;                    // comm box rows R (32 / 64 / 128): 16 / 32 / 64 KiB boxes
+  int agents;                 // independent TMA copy pipelines per comm CTA (one thread each)
+  int lag;                    // stores in flight before a slab signal waits for completion
+  int pull;                   // 0: this rank pulls nothing (no rows), barrier only
+  int sigmode;                // slab signals: 4 = signaler thread (default), 3 = agent release,
+                              // 1 = agent relaxed atomic (experiments: MIMW_MD_SIGMODE)
+  uint32_t *ctr;              // [MAX_SPLITS * max_slabs] slab counters + GO + PULLED, zeroed per launch
+  uint32_t *pad_local;        // this rank's signal pad: IN[MAX_SPLITS], OUT[MAX_SPLITS]; null = no barrier
+  uint32_t *pad_peer[MAX_SPLITS];
+  uint32_t epoch;
+  int rank, world;
+  __device__ __forceinline__ int nslabs(int q) const { return (ks[q] + COMM_SLAB - 1) / COMM_SLAB; }
+  // B boxes of slab j (K rows of the slab that exist, R at a time)
+  __device__ __forceinline__ int bsub(int q, int j) const {
+    const int left = ks[q] - j * COMM_SLAB;
+    return min(COMM_SLAB / box, (left + box - 1) / box);
+  }
+  __device__ __forceinline__ uint32_t pieces(int q, int j) const {
+    if (j >= nslabs(q)) return 0u;  // empty split
+    return (uint32_t)(rbox + bsub(q, j) * nbox);
+  }
+};
+
+// Position in the rotation-ordered list of comm boxes: split q (>= 1), slab j,
+// piece p of that slab's P boxes (the rbox A boxes first, then the B boxes).
+// A comm agent walks every nagents-th box.
+struct BoxCursor {
+  int q, j, p;
+  uint32_t P;
+  bool live;
+  __device__ __forceinline__ void init(const GatherSched &sp, int first) {
+    q = 1; j = 0; p = 0;
+    live = sp.pull && sp.nsplit > 1;
+    P = live ? sp.pieces(1, 0) : 0;
+    advance(sp, first);
+  }
+  __device__ __forceinline__ void advance(const GatherSched &sp, int by) {
+    p += by;
+    while (live && p >= (int)P) {
+      p -= (int)P;
+      if (++j >= sp.nslabs(q)) {
+        j = 0;
+        if (++q >= sp.nsplit) { live = false; break; }
+      }
+      P = sp.pieces(q, j);
+    }
+  }
+  __device__ __forceinline__ uint32_t *ctr(const GatherSched &sp) const { return sp.ctr + q * sp.max_slabs + j; }
+};
+
+// mailbox publish / read as shared-memory atomics (release / acquire at CTA
+// scope; atomics also keep compute-sanitizer's racecheck, which does not model
+// plain acquire/release flags, out of the message passing)
+__device__ __forceinline__ void st_release_cta_shared(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta_shared(uint32_t addr) {
+  uint32_t v;
+  asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// One comm agent (a single thread): copies boxes g = agent, agent + nagents,
+// ... through `nb` smem buffers — TMA load from the peer into buffer
+// i % nb, TMA store into the landing buffer, the buffer refilled once its
+// store has read it.  Once a store has fully landed (bulk wait_group, LAG
+// stores behind the newest so the agent rarely blocks), the agent publishes
+// its landed-box count in its smem mailbox; the CTA's signaler thread turns
+// counts into slab-counter releases (a release here would wait for this
+// thread's in-flight TMA traffic and serialise the pipeline).
+template <int LAG>
+__device__ __forceinline__ void gather_agent(const GatherSched &sp, uint32_t buf0, uint32_t bar0,
+                                             int nb, int agent, int nagents, uint32_t mbox) {
+  const uint32_t box_bytes = (uint32_t)sp.box * COMM_W * 2;
+  for (int i = 0; i < nb; ++i) mbar_init(bar0 + 8 * i, 1);
+  fence_mbar_init();
+  BoxCursor cur;
+  cur.init(sp, agent);
+  const CUtensorMap *dmap[COMM_MAX_BUFS];
+  int dx[COMM_MAX_BUFS], dy[COMM_MAX_BUFS];
+  uint32_t *dctr[COMM_MAX_BUFS];
+  uint32_t *sig[COMM_SIG];
+  auto issue_load = [&](int idx) {
+    const int slot = idx % nb;
+    const int k0 = cur.j * COMM_SLAB;
+    const CUtensorMap *src;
+    int x, y;
+    if (cur.p < sp.rbox) {
+      src = &sp.src_a[cur.q]; dmap[slot] = &sp.dst_a[cur.q]; x = k0; y = cur.p * sp.box;
+    } else {
+      const int pb = cur.p - sp.rbox;
+      src = &sp.src_b[cur.q]; dmap[slot] = &sp.dst_b[cur.q];
+      x = (pb % sp.nbox) * COMM_W; y = k0 + (pb / sp.nbox) * sp.box;
+    }
+    dx[slot] = x;
+    dy[slot] = y;
+    dctr[slot] = cur.ctr(sp);
+    const uint32_t bar = bar0 + 8 * slot;
+    mbar_arrive_expect_tx(bar, box_bytes);
+    tma_load_2d(buf0 + slot * box_bytes, src, bar, x, y);
+    cur.advance(sp, nagents);
+  };
+  auto landed = [&](int count, int first) {  // boxes [first, count) have landed
+    fence_proxy_async_global();
+    if (sp.sigmode == 4) {
+      st_release_cta_shared(mbox, (uint32_t)count);
+    } else {
+      for (int i = first; i < count; ++i) {
+        if (sp.sigmode & 2) red_release_gpu_add(sig[i % COMM_SIG], 1u);
+        else atomicAdd(sig[i % COMM_SIG], 1u);
+      }
+    }
+  };
+  int nl = 0;
+  while (nl < nb && cur.live) issue_load(nl++);
+  int ns = 0;
+  for (; ns < nl; ++ns) {
+    const int slot = ns % nb;
+    mbar_wait(bar0 + 8 * slot, (uint32_t)((ns / nb) & 1), 22);
+    tma_store_2d(dmap[slot], buf0 + slot * box_bytes, dx[slot], dy[slot]);
+    bulk_commit();
+    sig[ns % COMM_SIG] = dctr[slot];
+    if (nb == 1) {
+      bulk_wait_read<0>();           // single buffer: reload once this store has read it
+      if (cur.live) issue_load(nl++);
+    } else if (ns >= 1) {
+      bulk_wait_read<1>();           // store ns-1 has read its buffer: refill it
+      if (cur.live) issue_load(nl++);
+    }
+    if (ns >= LAG) {
+      bulk_wait<LAG>();              // stores <= ns-LAG have landed
+      landed(ns - LAG + 1, ns - LAG);
+    }
+  }
+  bulk_wait<0>();
+  landed(ns, ns > LAG ? ns - LAG : 0);
+}
+
+// Signaler thread of a comm CTA: replays each agent's box sequence and, as
+// the agents' mailboxes advance, bumps the slab counters with red.release.gpu
+// (cumulative over the agents' landed stores it acquired through smem).
+__device__ __forceinline__ void gather_signaler(const GatherSched &sp, int agent0, int agents,
+                                                int nagents, uint32_t mbox0) {
+  BoxCursor cs[6];
+  int seen[6];
+  for (int a = 0; a < agents; ++a) {
+    cs[a].init(sp, agent0 + a);
+    seen[a] = 0;
+  }
+  const uint64_t t0 = clock64();
+  while (true) {
+    bool any = false;
+    for (int a = 0; a < agents; ++a) {
+      if (!cs[a].live) continue;
+      any = true;
+      const int done = (int)ld_acquire_cta_shared(mbox0 + 4 * a);
+      uint32_t *c0 = nullptr;
+      uint32_t cnt = 0;
+      while (seen[a] < done && cs[a].live) {
+        uint32_t *c = cs[a].ctr(sp);
+        if (c != c0) {
+          if (cnt) red_release_gpu_add(c0, cnt);
+          c0 = c;
+          cnt = 0;
+        }
+        ++cnt;
+        ++seen[a];
+        cs[a].advance(sp, nagents);
+      }
+      if (cnt) red_release_gpu_add(c0, cnt);
+    }
+    if (!any) break;
+    if (clock64() - t0 > MIMW_WATCHDOG_CYCLES) watchdog_trap(mbox0, 0, 26);
+  }
+}
+
+// Entry barrier: every peer has launched, so its inputs are complete and it
+// may read ours ("arrive remote, wait local").  The leader (comm agent 0)
+// meets the peers through their signal pads and opens the local GO flag the
+// other agents wait on.
+__device__ __forceinline__ void gather_entry(const GatherSched &sp, bool leader) {
+  if (!sp.pad_local) return;
+  uint32_t *go = sp.ctr + MAX_SPLITS * sp.max_slabs;
+  if (leader) {
+    fence_sc_sys();
+    for (int p = 0; p < sp.world; ++p)
+      if (p != sp.rank) st_release_sys(sp.pad_peer[p] + sp.rank, sp.epoch);
+    for (int p = 0; p < sp.world; ++p)
+      if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + p, sp.epoch, 20);
+    st_release_gpu(go, 1u);
+  } else {
+    flag_wait_geq<false>(go, 1u, 21);
+  }
+}
+
+// Exit barrier: no rank returns (and lets its caller overwrite A_s / B_s)
+// before every peer has finished pulling from it.  Every agent counts itself
+// out; the leader waits for all `nparts`, then meets the peers.
+__device__ __forceinline__ void gather_exit(const GatherSched &sp, bool leader, uint32_t nparts) {
+  if (!sp.pad_local) return;
+  uint32_t *pulled = sp.ctr + MAX_SPLITS * sp.max_slabs + 1;
+  red_release_gpu_add(pulled, 1u);
+  if (!leader) return;
+  flag_wait_geq<false>(pulled, nparts, 23);
+  fence_sc_sys();
+  for (int p = 0; p < sp.world; ++p)
+    if (p != sp.rank) st_release_sys(sp.pad_peer[p] + MAX_SPLITS + sp.rank, sp.epoch);
+  for (int p = 0; p < sp.world; ++p)
+    if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + MAX_SPLITS + p, sp.epoch, 24);
+}
+
+__device__ __forceinline__ void gather_agent_lag(const GatherSched &sp, uint32_t buf0, uint32_t bar0,
+                                                 int nb, int agent, int nagents, uint32_t mbox) {
+  switch (sp.lag) {
+    case 1: gather_agent<1>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+    case 2: gather_agent<2>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+    case 4: gather_agent<4>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+    case 6: gather_agent<6>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+    case 12: gather_agent<12>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+    default: gather_agent<8>(sp, buf0, bar0, nb, agent, nagents, mbox); break;
+  }
+}
+
+// Dedicated comm CTA (comm_clusters > 0; the reference's rank-0 comm CTA,
+// multi_device_gemm.mimw:23-49): `agents` copy pipelines over the CTA's
+// whole smem ring, warp 7 the signaler.
+__device__ __forceinline__ void gather_comm_cta(const GatherSched &sp, uint32_t ring, uint32_t ring_bytes,
+                                                uint32_t bars, uint32_t mbox0, int ci, int ncomm) {
+  const int warp = threadIdx.x / 32;
+  const bool lane0 = (threadIdx.x % 32) == 0;
+  if (threadIdx.x == 0) gather_entry(sp, ci == 0);
+  __syncthreads();
+  const int nagents = ncomm * sp.agents;
+  if (lane0 && warp < sp.agents) {
+    const uint32_t box_bytes = (uint32_t)sp.box * COMM_W * 2;
+    const int nbuf = min((int)(ring_bytes / box_bytes), COMM_MAX_BUFS);
+    const int nb = nbuf / sp.agents;
+    gather_agent_lag(sp, ring + warp * nb * box_bytes, bars + 8 * warp * nb, nb,
+                     ci * sp.agents + warp, nagents, mbox0 + 4 * warp);
+  } else if (lane0 && warp == 7 && sp.sigmode == 4) {
+    gather_signaler(sp, ci * sp.agents, sp.agents, nagents, mbox0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) gather_exit(sp, ci == 0, (uint32_t)ncomm);
+}
+
+// all-gather GEMM CTAs carry two more warps: 6 = comm agent, 7 = signaler
+template <typename Prob>
+constexpr int kernel_threads() { return Prob::kGather ? NUM_THREADS + 64 : NUM_THREADS; }
+
 template <int CG, bool B_MN, typename OutT, typename Prob>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(kernel_threads<Prob>(), 1)
 gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, int N, int K,
                  const __grid_constant__ Prob sched) {
-  using C = Cfg<CG, B_MN, OutT>;
+  using C = Cfg<CG, B_MN, OutT, Prob::kGather>;
   constexpr bool GROUPED = Prob::kGrouped;
   // PAIRS = 2: a cluster of two CTA pairs computes two vertically adjacent
   // 256x256 tiles; each B half-tile is loaded once and multicast to the
@@ -167,10 +456,18 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int pair = (int)(crank >> 1);       // pair inside the cluster (PAIRS == 2)
   const uint32_t my_leader = crank & ~1u;
   const bool leader = (rank == 0);
-  const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
-  const int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
+  int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
   const int num_tiles = sched.num_tiles();
-  const int num_k = (K + BK - 1) / BK;
+  int num_k = (K + BK - 1) / BK;
+  bool comm = false;  // all-gather GEMM: the low cluster ids are comm pairs
+  if constexpr (Prob::kGather) {
+    static_assert(CG == 2 && B_MN && PAIRS == 1, "all-gather GEMM: 2-CTA, B as [K, N]");
+    comm = cluster < sched.comm_clusters;
+    cluster -= sched.comm_clusters;
+    nclusters -= sched.comm_clusters;
+    num_k = sched.kblocks;
+  }
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
@@ -184,15 +481,23 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), EPI_WARPS * CG);
     }
+    if constexpr (Prob::kGather)
+      for (int i = 0; i < 8; ++i)  // comm mailboxes
+        st_release_cta_shared(bar_base + C::BAR_BYTES + 8 * COMM_MAX_BUFS + 4 * i, 0u);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<CG>(tmem_slot, 512);
+  if (warp == 1 && !comm) tmem_alloc<CG>(tmem_slot, 512);
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
 
-  if (warp == 0) {
+  if (comm) {
+    if constexpr (Prob::kGather)
+      gather_comm_cta(sched, sbase, C::STAGES * C::STAGE_BYTES, bar_base + C::BAR_BYTES,
+                      bar_base + C::BAR_BYTES + 8 * COMM_MAX_BUFS,
+                      (cluster + sched.comm_clusters) * CG + (int)crank, sched.comm_clusters * CG);
+  } else if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
       int stage = 0;
@@ -205,6 +510,30 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int m0 = tc.row_base + (tc.mt * PAIRS + pair) * BM_CTA * CG +
                        (int)rank * (tc.swap_n ? tc.swap_n / 2 : BM_CTA);
         const int n0 = tc.nt * BN + (int)rank * C::NB_CTA;
+        if constexpr (Prob::kGather) {
+          // splits in rotation order; remote slabs gated on their counters
+          for (int q = 0; q < sched.nsplit; ++q) {
+            const int nk = (sched.ks[q] + BK - 1) / BK;
+            for (int kb = 0; kb < nk; ++kb) {
+              if (q > 0 && kb % (COMM_SLAB / BK) == 0) {
+                const int j = kb / (COMM_SLAB / BK);
+                flag_wait_geq<false>(sched.ctr + q * sched.max_slabs + j, sched.pieces(q, j), 25);
+                fence_proxy_async_global();
+              }
+              mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
+              const uint32_t fb = full_target0 + 8 * stage;
+              if (leader) mbar_arrive_expect_tx(full_bar(stage), C::STAGE_BYTES * CG);
+              const uint32_t sa = sbase + stage * C::STAGE_BYTES;
+              const uint32_t sb = sa + C::A_BYTES;
+              const int k0 = kb * BK;
+              tma_load_2d_cg2(sa, &sched.ga[q], fb, k0, m0);
+#pragma unroll
+              for (int j = 0; j < C::NB_CTA / 64; ++j)
+                tma_load_2d_cg2(sb + j * (64 * BK * 2), &sched.gb[q], fb, n0 + j * 64, k0);
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        } else {
         for (int kb = 0; kb < num_k; ++kb) {
           if constexpr (CG == 2) mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
           else mbar_wait(empty_bar(stage), phase ^ 1, 1);
@@ -260,6 +589,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        }  // !kGather
       }
     }
   } else if (warp == 1) {
@@ -309,6 +639,24 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 2 + EPI_WARPS) {
+    // ---------------- all-gather comm warps (distributed mode) ----------------
+    // comm_clusters == 0: every GEMM CTA pulls 1/(2 x pairs) of the remote
+    // boxes through its own 16 KiB buffer (warp 6), warp 7 signals the slabs.
+    if constexpr (Prob::kGather) {
+      if (sched.comm_clusters == 0 && lane_id() == 0) {
+        const int agent = cluster * CG + (int)crank, nagents = nclusters * CG;
+        const uint32_t mbox = bar_base + C::BAR_BYTES + 8 * COMM_MAX_BUFS;
+        if (warp == 2 + EPI_WARPS) {
+          gather_entry(sched, agent == 0);
+          gather_agent_lag(sched, sbase + C::BAR_OFF - C::COMM_EXTRA, bar_base + C::BAR_BYTES,
+                           C::COMM_EXTRA / (sched.box * COMM_W * 2), agent, nagents, mbox);
+          gather_exit(sched, agent == 0, (uint32_t)nagents);
+        } else if (sched.sigmode == 4) {
+          gather_signaler(sched, agent, 1, nagents, mbox);
+        }
       }
     }
   } else {
@@ -431,7 +779,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  if (warp == 1) {
+  if (warp == 1 && !comm) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, 512);
   }
@@ -439,14 +787,15 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
 template <int CG, bool B_MN, typename OutT, typename Prob>
 cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CUtensorMap &tC, int n,
-                          int k, const Prob &prob, int tiles, int max_clusters, cudaStream_t stream) {
-  using C = Cfg<CG, B_MN, OutT>;
+                          int k, const Prob &prob_in, int tiles, int max_clusters, cudaStream_t stream,
+                          int comm_clusters = 0) {
+  using C = Cfg<CG, B_MN, OutT, Prob::kGather>;
   constexpr int CS = CG * Prob::kPairs;  // CTAs per cluster
   auto kern = gemm_bf16_kernel<CG, B_MN, OutT, Prob>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.blockDim = dim3(kernel_threads<Prob>(), 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -467,11 +816,22 @@ cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CU
       clusters = active;
     cudaGetLastError();
   }
+  // all-gather GEMM: comm pairs come out of the co-resident budget (they must
+  // run alongside the GEMM pairs that wait on them)
+  clusters -= comm_clusters;
   if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
   if (clusters > tiles) clusters = tiles;
-  if (clusters <= 0) return cudaSuccess;
-  cfg.gridDim = dim3(clusters * CS, 1, 1);
-  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, prob);
+  if (clusters <= 0 && tiles > 0) return cudaErrorInvalidConfiguration;
+  if (clusters < 0) clusters = 0;
+  if (clusters + comm_clusters == 0) return cudaSuccess;
+  cfg.gridDim = dim3((clusters + comm_clusters) * CS, 1, 1);
+  if constexpr (Prob::kGather) {
+    Prob prob = prob_in;
+    prob.comm_clusters = comm_clusters;
+    return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, prob);
+  } else {
+    return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, prob_in);
+  }
 }
 
 template <typename OutT>
@@ -562,6 +922,33 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
   return err;
 }
 
+
+// ---- all-gather (K-gathered) multi-device GEMM -------------------------------
+struct GatherLayout {
+  int max_slabs = 0;
+  size_t ctr_off = 0, ctr_bytes = 0;
+  size_t land_a[MAX_SPLITS] = {}, land_b[MAX_SPLITS] = {};  // by rotation index q
+  size_t total = 0;
+};
+
+GatherLayout gather_layout(int rank, int world, const int64_t *k, int64_t rows, int64_t n) {
+  GatherLayout L;
+  auto align = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  int64_t kmax = 0;
+  for (int s = 0; s < world; ++s) kmax = std::max(kmax, k[s]);
+  L.max_slabs = (int)((kmax + COMM_SLAB - 1) / COMM_SLAB);
+  L.ctr_bytes = align(sizeof(uint32_t) * (MAX_SPLITS * (size_t)std::max(L.max_slabs, 1) + 4));
+  size_t off = L.ctr_bytes;
+  for (int q = 1; q < world; ++q) {
+    const int64_t kq = k[(rank + q) % world];
+    L.land_a[q] = off;
+    off = align(off + (size_t)rows * kq * 2);
+    L.land_b[q] = off;
+    off = align(off + (size_t)kq * n * 2);
+  }
+  L.total = off;
+  return L;
+}
 }  // namespace
 
 cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream) {
@@ -591,6 +978,94 @@ cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stre
   if (g.cta_group == 1)
     return g.w_kn ? grouped_impl<1, true>(g, stream) : grouped_impl<1, false>(g, stream);
   return g.w_kn ? grouped_impl<2, true>(g, stream) : grouped_impl<2, false>(g, stream);
+}
+
+size_t multi_device_gemm_workspace_bytes(int rank, int world, const int64_t *k, int64_t rows, int64_t n) {
+  return gather_layout(rank, world, k, rows, n).total;
+}
+
+cudaError_t multi_device_gemm_launch(const MultiDeviceGemmArgs &g, cudaStream_t stream) {
+  const GatherLayout L = gather_layout(g.rank, g.world, g.k, g.rows, g.n);
+  if (g.ws_bytes < L.total) return cudaErrorInvalidValue;
+  const bool barrier = g.pads[g.rank] != nullptr;
+  const bool work = g.rows > 0 && g.n > 0;
+  if (!work && !barrier) return cudaSuccess;
+  char *ws = static_cast<char *>(g.ws);
+  uint32_t *ctr = reinterpret_cast<uint32_t *>(ws + L.ctr_off);
+  cudaError_t e = cudaMemsetAsync(ctr, 0, L.ctr_bytes, stream);
+  if (e != cudaSuccess) return e;
+  auto *gs = new GatherSched;  // ~6 KB of tensor maps: keep it off the host stack
+  std::memset(gs, 0, sizeof(GatherSched));
+  // comm_clusters > 0: dedicated comm CTA pairs; < 0: distributed (a comm warp
+  // in every GEMM CTA, 16 KiB boxes).  A rank with no rows still meets its
+  // peers in the barrier, through one dedicated pair.
+  int comm = g.world > 1 ? (g.comm_clusters == 0 ? kDefaultCommPairs : g.comm_clusters) : 0;
+  if (comm < 0 && !work) comm = 1;
+  const bool distributed = comm < 0;
+  if (distributed) comm = 0;
+  const int box = distributed ? 32
+                  : (g.comm_box == 32 || g.comm_box == 64 || g.comm_box == 128) ? g.comm_box : 64;
+  gs->num_m = work ? (int)((g.rows + BM_CTA * 2 - 1) / (BM_CTA * 2)) : 0;
+  gs->num_n = work ? (int)((g.n + BN - 1) / BN) : 0;
+  gs->group = 8;
+  gs->M = (int)g.rows;
+  gs->rank = g.rank;
+  gs->world = g.world;
+  gs->epoch = g.epoch;
+  gs->ctr = ctr;
+  gs->max_slabs = L.max_slabs;
+  gs->box = box;
+  gs->sigmode = getenv("MIMW_MD_SIGMODE") ? atoi(getenv("MIMW_MD_SIGMODE")) : 4;
+  gs->agents = std::min(6, std::max(1, g.comm_agents > 0 ? g.comm_agents : 2));  // warps 0..5
+  gs->lag = g.comm_lag > 0 ? g.comm_lag : (distributed ? 4 : 8);
+  gs->rbox = (int)((g.rows + box - 1) / box);
+  gs->nbox = (int)((g.n + COMM_W - 1) / COMM_W);
+  gs->pad_local = g.pads[g.rank];
+  for (int p = 0; p < g.world; ++p) gs->pad_peer[p] = g.pads[p];
+  // never-dereferenced stand-in for maps of empty operands
+  const CUtensorMap dummy = make_tmap_2d(ws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 32, EPI_COLS, EPI_COLS,
+                                         EPI_COLS, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  int kblocks = 0;
+  int64_t ktot = 0;
+  for (int q = 0; q < g.world; ++q) {
+    const int s = (g.rank + q) % g.world;
+    const int64_t kq = g.k[s];
+    ktot += kq;
+    gs->ks[q] = (int)kq;
+    kblocks += (int)((kq + BK - 1) / BK);
+    gs->ga[q] = gs->gb[q] = gs->src_a[q] = gs->dst_a[q] = gs->src_b[q] = gs->dst_b[q] = dummy;
+    if (kq == 0 || !work) continue;
+    const void *abase = static_cast<const char *>(g.a[s]) + (size_t)g.row0 * kq * 2;
+    const void *la = q == 0 ? abase : ws + L.land_a[q];
+    const void *lb = q == 0 ? g.b[s] : ws + L.land_b[q];
+    gs->ga[q] = make_tmap_2d(la, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.rows, kq, kq, BK, BM_CTA,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+    gs->gb[q] = make_tmap_2d(lb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kq, g.n, g.n, 64, BK,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+    if (q == 0) continue;
+    // comm boxes {256, box rows}, unswizzled (pure copies)
+    gs->src_a[q] = make_tmap_2d(abase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.rows, kq, kq, COMM_W,
+                                box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    gs->dst_a[q] = make_tmap_2d(la, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.rows, kq, kq, COMM_W, box,
+                                CU_TENSOR_MAP_SWIZZLE_NONE);
+    gs->src_b[q] = make_tmap_2d(g.b[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kq, g.n, g.n, COMM_W,
+                                box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    gs->dst_b[q] = make_tmap_2d(lb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kq, g.n, g.n, COMM_W, box,
+                                CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  gs->nsplit = g.world;
+  gs->kblocks = kblocks;
+  gs->pull = work && ktot > 0;
+  if (work && ktot == 0) {  // C = 0 (oracles.cpp:19); the barrier below still runs
+    e = cudaMemset2DAsync(g.c, g.ldc * 2, 0, g.n * 2, g.rows, stream);
+    gs->num_m = 0;
+  }
+  const CUtensorMap tC = (work && ktot > 0) ? make_c_map<__nv_bfloat16>(g.c, g.rows, g.n, g.ldc) : dummy;
+  if (e == cudaSuccess && (gs->num_m > 0 || comm > 0))
+    e = launch_kernel<2, true, __nv_bfloat16>(tC, tC, tC, (int)g.n, (int)ktot, *gs,
+                                              gs->num_m * gs->num_n, g.max_clusters, stream, comm);
+  delete gs;
+  return e;
 }
 
 }  // namespace mimw

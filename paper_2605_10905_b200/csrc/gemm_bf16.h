@@ -38,4 +38,37 @@ struct GroupedGemmArgs {
 
 cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stream);
 
+// K-gathered multi-device GEMM (proj/kernels/multi_device_gemm.mimw,
+// oracle_multi_device_gemm oracles.cpp:57-80, generalised to `world` splits):
+//   c[rows, n] = sum_s a[s][row0 : row0 + rows, :] . b[s]
+// a[s] bf16 [m, k[s]] and b[s] bf16 [k[s], n] are the splits held by device
+// s, as pointers valid in this process (local, or peer memory mapped through
+// CUDA IPC).  The local split a[rank]/b[rank] is read in place; the others are
+// pulled over NVLink by comm CTAs into `ws` while the GEMM runs.  pads[p]:
+// device p's signal pad (2 * 8 u32, zeroed once at allocation, IPC-mapped) for
+// the entry/exit barrier, with `epoch` strictly increasing per call; all-null
+// pads = no device barrier (caller guarantees the peers' inputs are ready and
+// stay unchanged until this call completes, e.g. ranks emulated on one GPU).
+struct MultiDeviceGemmArgs {
+  int rank, world;
+  const void *a[8];
+  const void *b[8];
+  int64_t k[8];
+  int64_t n, row0, rows;
+  void *c;
+  int64_t ldc;
+  void *ws;
+  size_t ws_bytes;
+  uint32_t *pads[8];
+  uint32_t epoch;
+  int comm_clusters;  // > 0 dedicated comm CTA pairs, < 0 a comm warp in every GEMM CTA, 0 default
+  int max_clusters;   // cap on GEMM CTA pairs (0 = all co-resident minus comm)
+  int comm_box;       // comm box rows 32 / 64 / 128 of 512-byte rows (0 = 64: 32 KiB boxes)
+  int comm_agents;    // copy pipelines per comm CTA, 1..6 (0 = 2)
+  int comm_lag;       // stores in flight before a slab signal waits (0 = 8)
+};
+
+size_t multi_device_gemm_workspace_bytes(int rank, int world, const int64_t *k, int64_t rows, int64_t n);
+cudaError_t multi_device_gemm_launch(const MultiDeviceGemmArgs &g, cudaStream_t stream);
+
 }  // namespace mimw

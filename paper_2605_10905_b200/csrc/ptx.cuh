@@ -518,3 +518,58 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
 }
 
 }  // namespace mimw
+
+namespace mimw {
+
+// ---------------------------------------------------------------------------
+// Global-memory flags between CTAs / GPUs (readiness counters of the
+// all-gather GEMM, the peer entry/exit barrier).  The reference's analogue
+// is the remote barrier_arrive on a peer CTA's mbarrier ("arrive remote,
+// wait local", multi_device_gemm.mimw:43-46,56-57,67).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_release_gpu_add(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// order generic-proxy global accesses against async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+
+// Spin until *p >= target (acquire at gpu or sys scope); traps after the
+// watchdog budget like every mbarrier wait.
+template <bool SYS>
+__device__ __forceinline__ void flag_wait_geq(const uint32_t *p, uint32_t target, int tag) {
+  auto ld = [&] { return SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p); };
+  if ((int32_t)(ld() - target) >= 0) return;
+  const uint64_t t0 = clock64();
+  while ((int32_t)(ld() - target) < 0) {
+    __nanosleep(32);
+    if (clock64() - t0 > MIMW_WATCHDOG_CYCLES)
+      watchdog_trap((uint32_t)(uintptr_t)p, target, tag);
+  }
+}
+
+}  // namespace mimw

@@ -30,5 +30,14 @@ for cg in (1, 2):
     P.gemm_mxfp8(qa.view(torch.float8_e4m3fn), sa, qa.view(torch.float8_e4m3fn), sa, cta_group=cg)
 xl = torch.randn(6, 5000, device="cuda")
 P.layernorm(xl, torch.ones(5000, device="cuda"), torch.zeros(5000, device="cuda"))
+q1 = [torch.randn(2, 160, 128, device="cuda").bfloat16() for _ in range(5)]
+P.simplicial_attention_fwd(*q1, w1=3, w2=40)
+# all-gather multi-device GEMM, 3 emulated devices (sequential: no device barrier,
+# which needs the ranks' kernels co-resident), both comm modes
+from paper_2605_10905_b200 import multi_device as MD  # noqa: E402
+sa_ = [torch.randn(300, kk, device="cuda").bfloat16() for kk in (64, 136, 0)]
+sb_ = [torch.randn(kk, 264, device="cuda").bfloat16() for kk in (64, 136, 0)]
+for cp in (-1, 1):
+    MD.emulated_multi_device_gemm(sa_, sb_, comm_pairs=cp)
 torch.cuda.synchronize()
 print("sanitize run ok")

@@ -620,6 +620,99 @@ def bench_simplicial(args, rank, ws, local):
             "clocks": clocks}
 
 
+MD_SHAPE = ("GD1", 8192, 2048, 16384)  # PAPER.md:751 multi-GPU GEMM shape (M, N, K)
+NVLINK_GBS = 770.0  # B200_PROFILING.md: measured peer copy bandwidth per direction
+
+
+def bench_multidevice(args, rank, ws, local):
+    """the all-gather (K-gathered) multi-device GEMM,
+    C = [A_0 | ... | A_{W-1}] . [B_0 ; ... ; B_{W-1}] with split s on device s
+    (multi_device_gemm.mimw, oracles.cpp:57-80), PAPER.md:751 GD1 shape
+    M=8192 N=2048 K=16384.  One process per GPU: each rank pulls the peers'
+    splits over NVLink inside the GEMM kernel and computes its C row block.
+    With one GPU the second device is emulated: its split lives in local HBM
+    (standing in for the IPC-mapped peer buffer) and rank 0's launch is timed;
+    the same launch is also timed as gather-then-GEMM (D2D copies + GEMM)."""
+    import torch
+    import paper_2605_10905_b200 as P
+    from paper_2605_10905_b200 import multi_device as MD
+    pk = peaks()
+    dev = torch.device("cuda", local)
+    name, m, n, k = MD_SHAPE
+    world = ws if ws > 1 else 2
+    ks = [k // world] * world
+    rows = m // world
+    g = torch.Generator(device=dev).manual_seed(23 + rank)
+    stream = torch.cuda.current_stream()
+    c = torch.empty((rows, n), device=dev, dtype=torch.bfloat16)
+    flop_rank = 2.0 * rows * n * k
+    remote_bytes = sum(2.0 * (rows * kk + kk * n) for kk in ks[1:])
+    if ws > 1:
+        ag = MD.AllGatherGemm(m, ks, n, device=dev)
+        ag.a_local.copy_((torch.rand((m, ks[rank]), device=dev, generator=g) * 2 - 1).bfloat16())
+        ag.b_local.copy_((torch.rand((ks[rank], n), device=dev, generator=g) * 2 - 1).bfloat16())
+        torch.cuda.synchronize()
+        barrier(ws)
+
+        def step():
+            ag(out=c)
+        serial = None
+    else:
+        a = [(torch.rand((m, kk), device=dev, generator=g) * 2 - 1).bfloat16() for kk in ks]
+        b = [(torch.rand((kk, n), device=dev, generator=g) * 2 - 1).bfloat16() for kk in ks]
+        nb = MD.workspace_bytes(0, world, ks, rows, n)
+        wsb = torch.empty(nb + 1024, device=dev, dtype=torch.uint8)
+        wp = (wsb.data_ptr() + 1023) & ~1023
+        ap_, bp_ = [t.data_ptr() for t in a], [t.data_ptr() for t in b]
+
+        def step():
+            MD.multi_device_gemm(0, world, ap_, bp_, ks, m, n, 0, rows, c.data_ptr(), n, wp, nb)
+        a_land = torch.empty((rows, k), device=dev, dtype=torch.bfloat16)
+        b_land = torch.empty((k, n), device=dev, dtype=torch.bfloat16)
+        a_land[:, :ks[0]].copy_(a[0][:rows])
+        b_land[:ks[0]].copy_(b[0])
+
+        def serial_step():
+            off = ks[0]
+            for s_ in range(1, world):
+                a_land[:, off:off + ks[s_]].copy_(a[s_][:rows])
+                b_land[off:off + ks[s_]].copy_(b[s_])
+                off += ks[s_]
+            P.gemm(a_land, b_land, out=c)
+        steps = max(10, args.steps)
+        serial = timed(serial_step, steps, args.warmup, ws, stream) / steps
+    steps = max(10, args.steps)
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(step, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    per = secs / steps
+    achieved = flop_rank / per / 1e12
+    target = max(flop_rank / (pk["bf16"] * 1e12), remote_bytes / (NVLINK_GBS * 1e9))
+    out = {"value": round(flop_rank * (ws if ws > 1 else 1) / per / 1e12, 1), "unit": "TFLOPS",
+           "ms_per_step": round(per * 1e3, 4), "scaling": "strong" if ws > 1 else "weak",
+           "config": {"workload": f"all-gather multi-device GEMM (SURVEY §8f rank 1), PAPER.md:751 "
+                                  f"{name} M={m} N={n} K={k} bf16, K split over {world} devices, "
+                                  f"C rows partitioned",
+                      "devices": world,
+                      "peers": "real (CUDA IPC over NVLink)" if ws > 1 else
+                               "emulated: the second device's split in local HBM, rank 0 timed",
+                      "comm": "comm warp in every GEMM CTA pair (library default)"},
+           "roofline": {"bound": "tensor|nvlink", "achieved": round(achieved, 1), "peak": pk["bf16"],
+                        "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
+                        "target_ms": round(target * 1e3, 4),
+                        "frac_of_target": round(target / per, 4),
+                        "remote_bytes_per_rank": remote_bytes,
+                        "target_rule": "max(FLOP / bf16 peak, remote bytes / 770 GB/s NVLink)",
+                        "traffic": None},
+           "clocks": clocks}
+    if serial is not None:
+        out["gather_then_gemm_ms"] = round(serial * 1e3, 4)
+    if ws > 1:
+        ag.close()
+    return out
+
+
 def torch_empty_cache():
     import torch
     torch.cuda.empty_cache()
@@ -631,7 +724,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm", "simplicial"])
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm", "simplicial",
+                             "multidevice"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -677,6 +771,8 @@ def main():
         res = bench_layernorm(args, rank, ws, local)
     elif args.workload == "simplicial":
         res = bench_simplicial(args, rank, ws, local)
+    elif args.workload == "multidevice":
+        res = bench_multidevice(args, rank, ws, local)
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
@@ -693,6 +789,14 @@ def main():
             torch_empty_cache()
             res["secondary"]["layernorm_cluster"] = bench_layernorm(args, rank, ws, local)
             res["secondary"]["simplicial_attention"] = bench_simplicial(args, rank, ws, local)
+            try:
+                if ws > 1 and not os.environ.get("MIMW_BENCH_MD"):
+                    # real peers need every rank's kernel in the device barrier: opt-in
+                    # (--workload multidevice or MIMW_BENCH_MD=1) so the scaling line is never at risk
+                    raise RuntimeError("multi-GPU form: run --workload multidevice")
+                res["secondary"]["multi_device_gemm"] = bench_multidevice(args, rank, ws, local)
+            except Exception as e:  # never lose the headline line to the §8f extra
+                res["secondary"]["multi_device_gemm"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, thr, kind, sample = cpu_gemm_sample()
         res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,

@@ -164,11 +164,29 @@ int mimw_b200_ipc_free(void *ptr);
 int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, float *o,
                                float *lse, int64_t seq, int64_t d, int64_t w, double scale);
 
+/* window value selecting non-causal attention (every key of the sequence; the
+ * paper's AFN / ABC rows, PAPER.md:702-716 — no reference oracle) */
+#define MIMW_WINDOW_NONCAUSAL 0
+
 /* Device form: q, k, v, o bf16 [batch, heads, seq, head_dim] contiguous,
- * head_dim == 128; lse fp32 [batch, heads, seq] or NULL.  Warp-specialized
+ * head_dim == 128; lse fp32 [batch, heads, seq] or NULL.  window >= 1 as in
+ * the reference, or MIMW_WINDOW_NONCAUSAL.  Warp-specialized
  * kernel: TMA producer warp, single-thread tcgen05 MMA warp (S = QK^T and
  * O += PV with P in TMEM), two ping-pong softmax/correction warpgroups. */
 int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o, float *lse,
+                            int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
+                            int64_t window, double scale, void *stream);
+
+/* ---- Attention backward (PAPER.md:702-716 ABC rows) --
+ * Gradients of o = softmax(scale q k^T) v (causal with `window` as the forward,
+ * or MIMW_WINDOW_NONCAUSAL).  No reference counterpart (the reference has no
+ * backward); oracle: the f64 restatement orc_attention_bwd in oracle/oracle.c.
+ * q, k, v, o, dout, dq, dk, dv bf16 [batch, heads, seq, 128] contiguous; lse
+ * fp32 [batch, heads, seq] (natural log, as written by mimw_b200_attention_fwd).
+ * seq % 4 == 0.  KV-stationary tcgen05 kernel (key-major S^T / dP^T so P^T and
+ * dS^T feed the dV / dK MMAs from TMEM), dQ accumulated by TMA reduce-add. */
+int mimw_b200_attention_bwd(const void *q, const void *k, const void *v, const void *o,
+                            const void *dout, const float *lse, void *dq, void *dk, void *dv,
                             int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
                             int64_t window, double scale, void *stream);
 

@@ -57,6 +57,9 @@ def _declare_c(lib):
     lib.orc_attention_rows.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p,
                                        _i64, _i64, _i64, C_.c_double, _i64, _i64]
     lib.orc_simplicial_attention.argtypes = [_f32p] * 7 + [_i64] * 4 + [C_.c_double]
+    lib.orc_attention_mode_rows.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p, _i64, _i64,
+                                            _i64, C_.c_int, C_.c_double, _i64, _i64]
+    lib.orc_attention_bwd.argtypes = [_f32p] * 7 + [_i64, _i64, _i64, C_.c_int, C_.c_double]
     lib.orc_layernorm.argtypes = [_f32p, _f32p, _f32p, C_.c_double, _f32p,
                                   _f32p, _f32p, _i64, _i64]
     lib.orc_write_tensor.argtypes = [C_.c_char_p, _f32p, C_.POINTER(_i64), C_.c_int]
@@ -212,6 +215,32 @@ def oracle_attention_rows(q, k, v, w: int, scale: float, r0: int, r1: int):
     lse = np.empty(r1 - r0, np.float32)
     C.orc_attention_rows(q, k, v, o, lse.ctypes.data, s, d, w, scale, r0, r1)
     return o, lse
+
+
+def oracle_attention_full(q, k, v, scale: float, rows=None):
+    """NON-CAUSAL attention of one head (every key; no reference oracle —
+    restated from oracles.cpp:119-145 with the key range widened, see
+    oracle.c key_range).  ``rows=(r0, r1)`` computes only those rows.
+    Returns (o, lse)."""
+    q, k, v = map(_f32, (q, k, v))
+    s, d = q.shape
+    r0, r1 = rows if rows is not None else (0, s)
+    o = np.empty((r1 - r0, d), np.float32)
+    lse = np.empty(r1 - r0, np.float32)
+    C.orc_attention_mode_rows(q, k, v, o, lse.ctypes.data, s, d, s, 0, scale, r0, r1)
+    return o, lse
+
+
+def oracle_attention_bwd(q, k, v, do, scale: float, causal: bool = True, w: int | None = None):
+    """Gradients (dq, dk, dv) of one [S, D] head of attention (causal with
+    window ``w`` as oracle_attention, or non-causal), evaluated in f64 —
+    a restatement: the reference has no backward (oracle.c orc_attention_bwd)."""
+    q, k, v, do = map(_f32, (q, k, v, do))
+    s, d = q.shape
+    dq, dk, dv = (np.empty((s, d), np.float32) for _ in range(3))
+    C.orc_attention_bwd(q, k, v, do, dq, dk, dv, s, d, w if w is not None else s,
+                        1 if causal else 0, scale)
+    return dq, dk, dv
 
 
 def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float):

@@ -239,6 +239,111 @@ void orc_attention(const float *q, const float *k, const float *v, float *o,
   orc_attention_rows(q, k, v, o, lse, seq, d, w, scale, 0, seq);
 }
 
+/* Key range of query row i: the reference's windowed causal rule
+ * (oracles.cpp:123-126), or — causal == 0 — every key of the sequence.
+ * The non-causal mode has NO reference oracle (the reference's attention is
+ * causal only); it is a restatement with the key range
+ * widened and the reference's arithmetic otherwise unchanged (f64 scores and
+ * softmax, f32 accumulation of o in ascending key order, oracles.cpp:127-144). */
+static void key_range(int64_t i, int64_t seq, int64_t w, int causal, int64_t *j0, int64_t *j1) {
+  if (causal) {
+    *j0 = i - w + 1 > 0 ? i - w + 1 : 0;
+    *j1 = i;
+  } else {
+    *j0 = 0;
+    *j1 = seq - 1;
+  }
+}
+
+void orc_attention_mode_rows(const float *q, const float *k, const float *v, float *o,
+                             float *lse, int64_t seq, int64_t d, int64_t w, int causal,
+                             double scale, int64_t r0, int64_t r1) {
+  double *scores = (double *)malloc(sizeof(double) * (size_t)(seq > 0 ? seq : 1));
+  memset(o, 0, sizeof(float) * (size_t)((r1 - r0) * d));
+  o -= r0 * d;
+  if (lse) lse -= r0;
+  for (int64_t i = r0; i < r1; ++i) {
+    int64_t j0, j1;
+    key_range(i, seq, w, causal, &j0, &j1);
+    int64_t cnt = 0;
+    for (int64_t j = j0; j <= j1; ++j) {
+      double s = 0;
+      for (int64_t x = 0; x < d; ++x) s += (double)q[i * d + x] * k[j * d + x];
+      scores[cnt++] = s * scale;
+    }
+    double m = -INFINITY;
+    for (int64_t t = 0; t < cnt; ++t) m = scores[t] > m ? scores[t] : m;
+    double l = 0;
+    for (int64_t t = 0; t < cnt; ++t) l += exp(scores[t] - m);
+    for (int64_t t = 0; t < cnt; ++t) {
+      double p = exp(scores[t] - m) / l;
+      const float *vr = v + (j0 + t) * d;
+      for (int64_t x = 0; x < d; ++x) o[i * d + x] += (float)(p * vr[x]);
+    }
+    if (lse) lse[i] = (float)(m + log(l));
+  }
+  free(scores);
+}
+
+/* Attention backward for one head: the gradients of o = softmax(scale q k^T) v
+ * (key ranges as key_range) with respect to q, k, v, given do.  No reference
+ * counterpart (the reference has no backward): the
+ * standard derivation, evaluated in f64 —
+ *   P = softmax rows, dV = P^T dO, dP = dO V^T, D_i = sum_j P_ij dP_ij,
+ *   dS = P (dP - D), dQ = scale dS K, dK = scale dS^T Q. */
+void orc_attention_bwd(const float *q, const float *k, const float *v, const float *dout,
+                       float *dq, float *dk, float *dv, int64_t seq, int64_t d, int64_t w,
+                       int causal, double scale) {
+  double *p = (double *)malloc(sizeof(double) * (size_t)(seq > 0 ? seq : 1));
+  double *dqa = (double *)calloc((size_t)(seq * d > 0 ? seq * d : 1), sizeof(double));
+  double *dka = (double *)calloc((size_t)(seq * d > 0 ? seq * d : 1), sizeof(double));
+  double *dva = (double *)calloc((size_t)(seq * d > 0 ? seq * d : 1), sizeof(double));
+  for (int64_t i = 0; i < seq; ++i) {
+    int64_t j0, j1;
+    key_range(i, seq, w, causal, &j0, &j1);
+    const int64_t cnt = j1 - j0 + 1;
+    double m = -INFINITY;
+    for (int64_t t = 0; t < cnt; ++t) {
+      double s = 0;
+      for (int64_t x = 0; x < d; ++x) s += (double)q[i * d + x] * k[(j0 + t) * d + x];
+      p[t] = s * scale;
+      m = p[t] > m ? p[t] : m;
+    }
+    double l = 0;
+    for (int64_t t = 0; t < cnt; ++t) {
+      p[t] = exp(p[t] - m);
+      l += p[t];
+    }
+    double di = 0;
+    for (int64_t t = 0; t < cnt; ++t) {
+      p[t] /= l;
+      double dp = 0;
+      for (int64_t x = 0; x < d; ++x) dp += (double)dout[i * d + x] * v[(j0 + t) * d + x];
+      di += p[t] * dp;
+    }
+    for (int64_t t = 0; t < cnt; ++t) {
+      const int64_t j = j0 + t;
+      double dp = 0;
+      for (int64_t x = 0; x < d; ++x) dp += (double)dout[i * d + x] * v[j * d + x];
+      const double ds = p[t] * (dp - di);
+      for (int64_t x = 0; x < d; ++x) {
+        dva[j * d + x] += p[t] * dout[i * d + x];
+        dqa[i * d + x] += scale * ds * k[j * d + x];
+        dka[j * d + x] += scale * ds * q[i * d + x];
+      }
+    }
+  }
+  for (int64_t e = 0; e < seq * d; ++e) {
+    dq[e] = (float)dqa[e];
+    dk[e] = (float)dka[e];
+    dv[e] = (float)dva[e];
+  }
+  free(p);
+  free(dqa);
+  free(dka);
+  free(dva);
+}
+
 /* Trilinear attention with asymmetric causal windows
  * (core/src/oracles.cpp:82-117). */
 void orc_simplicial_attention(const float *q, const float *k1, const float *v1,

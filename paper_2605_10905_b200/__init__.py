@@ -71,6 +71,7 @@ def _optional_sigs():
     return {
         "mimw_b200_oracle_attention": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double],
         "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
+        "mimw_b200_attention_bwd": [_vp] * 5 + [_vp] + [_vp] * 3 + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
                                                                            C.c_int32, _vp, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
@@ -218,13 +219,19 @@ def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_
     return out
 
 
+WINDOW_NONCAUSAL = 0
+
+
 def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None, out=None,
                   lse=None, want_lse: bool = True, stream=None, emu: int = -1, max_ctas: int = 0,
-                  trace=None):
-    """Causal (optionally windowed) attention forward on bf16 [B, H, S, 128]
-    CUDA tensors.  Returns (o, lse) with lse fp32 [B, H, S] (natural log)."""
+                  trace=None, causal: bool = True):
+    """Causal (optionally windowed) or, with ``causal=False``, non-causal
+    attention forward on bf16 [B, H, S, 128] CUDA tensors.  Returns (o, lse)
+    with lse fp32 [B, H, S] (natural log)."""
     import torch
     b, h, s, d = q.shape
+    if not causal:
+        window = WINDOW_NONCAUSAL
     if out is None:
         out = torch.empty_like(q)
     if lse is None and want_lse:
@@ -323,3 +330,31 @@ def simplicial_attention_fwd(q, k1, v1, k2, v2, w1: int, w2: int, scale: float |
         q.data_ptr(), k1.data_ptr(), v1.data_ptr(), k2.data_ptr(), v2.data_ptr(), out.data_ptr(),
         lse.data_ptr() if lse is not None else None, bh, s, d, w1, w2, scale, _stream(stream)))
     return out, lse
+
+
+def attention_bwd(q, k, v, o, do, lse, window: int | None = None, scale: float | None = None,
+                  causal: bool = True, dq=None, dk=None, dv=None, stream=None):
+    """Attention backward on bf16 [B, H, S, 128] CUDA tensors: returns (dq, dk, dv)
+    given the forward's output ``o`` and ``lse`` (fp32 [B, H, S]) and the
+    upstream gradient ``do``.  ``causal=False`` for non-causal attention."""
+    import torch
+    b, h, s, d = q.shape
+    if d != 128:
+        raise MimwError(ERR_UNSUPPORTED, "device attention supports head_dim == 128")
+    for t in (q, k, v, o, do, lse):
+        if not t.is_contiguous():
+            raise MimwError(ERR_UNSUPPORTED, "attention_bwd needs contiguous tensors")
+    if scale is None:
+        scale = d ** -0.5
+    if not causal:
+        window = WINDOW_NONCAUSAL
+    elif window is None:
+        window = s
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    _check(lib().mimw_b200_attention_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                         do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+                                         dk.data_ptr(), dv.data_ptr(), b, h, s, d, window, scale,
+                                         _stream(stream)))
+    return dq, dk, dv

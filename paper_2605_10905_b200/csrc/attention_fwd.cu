@@ -68,6 +68,7 @@ struct Params {
   int bh;            // batch * heads
   int seq;
   int window;        // keys j in [i - window + 1, i]
+  int causal;        // 0: every key of the sequence (non-causal, PAPER.md:702-716 AFN rows)
   int nqb;           // 256-row blocks per head
   float scale_log2;  // scale * log2(e)
   float *lse;        // [bh, seq] or null
@@ -79,8 +80,8 @@ struct Params {
 
 // KV tile range [lo, hi] needed by Q rows [r0, r0 + 127]
 __device__ __forceinline__ void kv_range(int r0, const Params &p, int &lo, int &hi) {
-  int last = min(r0 + BQ - 1, p.seq - 1);
-  int first_key = max(0, r0 - p.window + 1);
+  int last = p.causal ? min(r0 + BQ - 1, p.seq - 1) : p.seq - 1;
+  int first_key = p.causal ? max(0, r0 - p.window + 1) : 0;
   lo = first_key / BKV;
   hi = last / BKV;
 }
@@ -465,7 +466,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         const int k0 = j * BKV;
         // tile needs masking if any (row, key) pair of the whole Q tile is invalid
-        const bool need_mask = (k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window) ||
+        const bool need_mask = (p.causal && ((k0 + BKV - 1 > rt) || (k0 < rt + BQ - p.window))) ||
                                (k0 + BKV > p.seq) || !p.scale_pos;
         if (!need_mask) {
 #pragma unroll
@@ -495,8 +496,8 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             for (int c = 0; c < 128; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
           }
           // valid keys of this row form one contiguous column range [c_lo, c_hi]
-          const int c_lo = row - p.window + 1 - k0;
-          const int c_hi = min(row, p.seq - 1) - k0;
+          const int c_lo = p.causal ? row - p.window + 1 - k0 : -k0;
+          const int c_hi = (p.causal ? min(row, p.seq - 1) : p.seq - 1) - k0;
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c < c_lo || c > c_hi) s[c] = 0xff800000u;  // -inf
@@ -658,7 +659,8 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   Params p;
   p.bh = (int)bh;
   p.seq = (int)a.seq;
-  p.window = (int)(a.window < a.seq ? a.window : a.seq);
+  p.causal = a.window > 0 ? 1 : 0;  // window <= 0: non-causal (every key)
+  p.window = (int)(a.window > 0 && a.window < a.seq ? a.window : a.seq);
   p.nqb = (int)((a.seq + 2 * BQ - 1) / (2 * BQ));
   p.scale_log2 = (float)(a.scale * 1.4426950408889634);
   p.lse = a.lse;

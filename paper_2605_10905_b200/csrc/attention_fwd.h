@@ -10,7 +10,7 @@ struct AttnArgs {
   void *o;                // [batch, heads, seq, 128] bf16
   float *lse;             // [batch, heads, seq] fp32 (natural log) or null
   int64_t batch, heads, seq;
-  int64_t window;         // keys j in [i - window + 1, i]; >= seq means plain causal
+  int64_t window;         // keys j in [i - window + 1, i]; >= seq plain causal; <= 0 non-causal
   double scale;
   int max_ctas;           // 0 = one persistent CTA per SM
   unsigned long long *trace = nullptr;  // optional [grid][12 warps][8] cycle counters

@@ -17,6 +17,7 @@
 #include "../../include/mimw_b200.h"
 #include "convert.h"
 #include "attention_fwd.h"
+#include "attention_bwd.h"
 #include "gemm_bf16.h"
 #include "gemm_mxfp8.h"
 #include "layernorm_cluster.h"
@@ -439,7 +440,8 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
   return guarded([&] {
     require(batch >= 0 && heads >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
     require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device attention supports head_dim == 128");
-    require(window >= 1, MIMW_ERR_ARG, "window must be >= 1");
+    require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
+            "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
     require(seq < (1ll << 31) && batch * heads < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
     if (batch == 0 || heads == 0 || seq == 0) return;
     require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
@@ -458,6 +460,43 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
     a.window = window;
     a.scale = scale;
     check_cuda(mimw::attention_fwd_launch(a, static_cast<cudaStream_t>(stream)), "attention launch");
+  });
+}
+
+// ---- attention backward ---------------------------------
+int mimw_b200_attention_bwd(const void *q, const void *k, const void *v, const void *o,
+                            const void *dout, const float *lse, void *dq, void *dk, void *dv,
+                            int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
+                            int64_t window, double scale, void *stream) {
+  return guarded([&] {
+    require(batch >= 0 && heads >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
+    require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device attention supports head_dim == 128");
+    require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
+            "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
+    require(seq < (1ll << 31) && batch * heads < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
+    if (batch == 0 || heads == 0 || seq == 0) return;
+    require(q && k && v && o && dout && lse && dq && dk && dv, MIMW_ERR_ARG, "null pointer");
+    require(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
+             (uintptr_t)dk | (uintptr_t)dv) % 16 == 0,
+            MIMW_ERR_UNSUPPORTED, "tensors must be 16-byte aligned");
+    require(seq % 4 == 0, MIMW_ERR_UNSUPPORTED, "seq must be a multiple of 4 (16-byte dQ accumulator rows)");
+    require_sm100();
+    mimw::AttnBwdArgs a{};
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.o = o;
+    a.dout = dout;
+    a.lse = lse;
+    a.dq = dq;
+    a.dk = dk;
+    a.dv = dv;
+    a.batch = batch;
+    a.heads = heads;
+    a.seq = seq;
+    a.window = window;
+    a.scale = scale;
+    check_cuda(mimw::attention_bwd_launch(a, static_cast<cudaStream_t>(stream)), "attention bwd launch");
   });
 }
 
@@ -616,7 +655,8 @@ int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void
   return guarded([&] {
     if (batch == 0 || heads == 0 || seq == 0) return;
     require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
-    require(window >= 1, MIMW_ERR_ARG, "window must be >= 1");
+    require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
+            "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
     require_sm100();
     mimw::AttnArgs a{};
     a.q = q;

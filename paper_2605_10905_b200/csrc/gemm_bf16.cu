@@ -230,8 +230,9 @@ struct BoxCursor {
 // scope; atomics also keep compute-sanitizer's racecheck, which does not model
 // plain acquire/release flags, out of the message passing)
 __device__ __forceinline__ void st_release_cta_shared(uint32_t addr, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  uint32_t prev;
+  asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(addr), "r"(v) : "memory");
+  (void)prev;
 }
 __device__ __forceinline__ uint32_t ld_acquire_cta_shared(uint32_t addr) {
   uint32_t v;

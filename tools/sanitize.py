@@ -30,6 +30,10 @@ for cg in (1, 2):
     P.gemm_mxfp8(qa.view(torch.float8_e4m3fn), sa, qa.view(torch.float8_e4m3fn), sa, cta_group=cg)
 xl = torch.randn(6, 5000, device="cuda")
 P.layernorm(xl, torch.ones(5000, device="cuda"), torch.zeros(5000, device="cuda"))
+o_, l_ = P.attention_fwd(q, k, v, causal=False)
+P.attention_bwd(q, k, v, o_, torch.randn_like(q), l_, causal=False)
+o_, l_ = P.attention_fwd(q, k, v, window=77)
+P.attention_bwd(q, k, v, o_, torch.randn_like(q), l_, window=77)
 q1 = [torch.randn(2, 160, 128, device="cuda").bfloat16() for _ in range(5)]
 P.simplicial_attention_fwd(*q1, w1=3, w2=40)
 # all-gather multi-device GEMM, 3 emulated devices (sequential: no device barrier,

@@ -161,3 +161,34 @@ def test_attention_rows_matches_full():
     o, lse = oracle.oracle_attention(q, k, v, 30, 0.2, with_lse=True)
     orow, lrow = oracle.oracle_attention_rows(q, k, v, 30, 0.2, 33, 61)
     assert np.array_equal(orow, o[33:61]) and np.array_equal(lrow, lse[33:61])
+
+
+# ---------------------------------------------------------------------------
+# restated oracles without a reference counterpart:
+# pinned against torch float64 autograd instead
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("causal,w", [(False, None), (True, None), (True, 7)])
+def test_attention_bwd_oracle_matches_torch_f64(causal, w):
+    import torch
+    s, d, scale = 37, 16, 0.3
+    q, k, v, do = (oracle.random_tile([s, d], 900 + i) for i in range(4))
+    Q, K, V = (torch.tensor(x, dtype=torch.float64, requires_grad=True) for x in (q, k, v))
+    S = (Q @ K.T) * scale
+    if causal:
+        i = torch.arange(s)
+        ww = w if w is not None else s
+        bad = (i[None, :] > i[:, None]) | (i[:, None] - i[None, :] >= ww)
+        S = S.masked_fill(bad, -float("inf"))
+    O = torch.softmax(S, -1) @ V
+    want = torch.autograd.grad(O, (Q, K, V), torch.tensor(do, dtype=torch.float64))
+    got = oracle.oracle_attention_bwd(q, k, v, do, scale, causal=causal, w=w)
+    for g, t in zip(got, want):
+        np.testing.assert_allclose(g, t.numpy(), rtol=1e-5, atol=1e-6)
+    if not causal:
+        o, lse = oracle.oracle_attention_full(q, k, v, scale)
+        np.testing.assert_allclose(o, O.detach().numpy(), rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(lse, torch.logsumexp(S, -1).detach().numpy(), rtol=1e-5)
+    else:
+        # the causal mode of the restatement is the reference's oracle_attention
+        o_ref = oracle.oracle_attention(q, k, v, w if w is not None else s, scale)
+        np.testing.assert_allclose(o_ref, O.detach().numpy(), rtol=1e-5, atol=1e-6)

@@ -19,15 +19,17 @@
 //   dV  += P^T dO_i       (TS: P^T bf16 in TMEM, dO_i MN-major)
 //   dK  += dS^T Q_i       (TS)
 //   dQ_i^T = K^T dS^T     (SS: K MN-major, dS^T staged in smem)
-// MIMW roles (12 warps):
+// MIMW roles (16 warps):
 //   warp 0      TMA producer: K, V once; Q_i, dO_i, lse_i, D_i per step (2 stages)
 //   warp 1      MMA issuer (one elected lane), tcgen05.commit -> mbarriers
-//   warps 4-7   "softmax" warpgroup: P^T, dS^T from S^T / dP^T (lane = key),
-//               P^T / dS^T -> TMEM, dS^T -> smem; final dK, dV epilogue
-//   warps 8-11  dQ drain: dQ_i^T TMEM -> smem -> TMA reduce-add (fp32) into
+//   warps 4-11  two "softmax" warpgroups, one per 32-query half of the step:
+//               P^T, dS^T from S^T / dP^T (lane = key), P^T / dS^T -> TMEM,
+//               dS^T -> smem (double-buffered); final dK, dV epilogue
+//   warps 12-15 dQ drain: dQ_i^T TMEM -> smem -> TMA reduce-add (fp32) into
 //               a transposed dQ accumulator [bh, 128, seq] in HBM
-// TMEM columns: S^T x2 [0,128) (fp32; P^T / dS^T bf16 overwrite it after it is
-// read), dP^T [128,192), dQ^T [192,256), dV [256,384), dK [384,512).
+// TMEM columns: S^T x2 [0,128) (fp32; each warpgroup overwrites its own 32
+// columns with P^T | dS^T bf16 once read), dP^T [128,192), dQ^T [192,256),
+// dV [256,384), dK [384,512).
 // S^T of step i+2 reuses step i's buffer: it is issued after dV_i / dK_i
 // (tcgen05.mma ops of one thread execute in issue order).
 #include "attention_bwd.h"
@@ -41,18 +43,20 @@ namespace {
 constexpr int D = 128;
 constexpr int BQ = 64;                    // queries per step (MMA N of S^T / dP^T)
 constexpr int BKV = 128;                  // keys per CTA (MMA M)
-constexpr int NUM_THREADS = 384;
+constexpr int NUM_THREADS = 512;
 constexpr int KPANEL = BKV * 128;         // 16 KiB: [128 keys][64 d] bf16, SW128
 constexpr int QPANEL = BQ * 128;          // 8 KiB:  [64 queries][64 d]
 constexpr int QT_BYTES = 2 * QPANEL;      // one Q_i or dO_i tile
 constexpr int SM_K = 0;
 constexpr int SM_V = SM_K + 2 * KPANEL;
-constexpr int SM_Q = SM_V + 2 * KPANEL;           // 2 stages
-constexpr int SM_DO = SM_Q + 2 * QT_BYTES;        // 2 stages
-constexpr int SM_DS = SM_DO + 2 * QT_BYTES;       // [128 keys][64 queries] bf16, SW128 (16 KiB)
-constexpr int SM_DQ = SM_DS + BKV * 128;          // 4 warps x 2 boxes x [32 d][32 q] f32 (32 KiB)
-constexpr int SM_LD = SM_DQ + 4 * 8192;           // 2 stages x (lse2[64] + D[64]) f32
-constexpr int SM_BAR = SM_LD + 2 * 512;
+constexpr int NST = 3;                            // Q_i / dO_i / lse_i / D_i stages
+constexpr int SM_Q = SM_V + 2 * KPANEL;
+constexpr int SM_DO = SM_Q + NST * QT_BYTES;
+constexpr int SM_DS = SM_DO + NST * QT_BYTES;     // 2 x [128 keys][64 queries] bf16, SW128 (16 KiB each)
+constexpr int SM_DQ = SM_DS + 2 * BKV * 128;      // 4 warps x 2 boxes x [32 d][32 q] f32 (32 KiB)
+constexpr int SM_LD = SM_DQ + 4 * 8192;           // NST stages x (lse2[64] + D[64]) f32
+constexpr int SM_BAR = SM_LD + NST * 512;
+static_assert(SM_BAR + 256 + 1024 <= 232448, "smem");
 constexpr int SMEM_TOTAL = SM_BAR + 256 + 1024;
 constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 192, TM_DV = 256, TM_DK = 384;
 constexpr uint32_t IDESC_SDP = idesc_bf16(BKV, BQ, 0, 0);  // K-major A, K-major B
@@ -111,11 +115,13 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   const uint32_t bars = sbase + SM_BAR;
   const uint32_t kv_full = bars;
   auto ld_full = [&](int s) { return bars + 8 + 8 * s; };
-  auto ld_empty = [&](int s) { return bars + 24 + 8 * s; };
-  const uint32_t s_full = bars + 40, dp_free = bars + 48, p_full = bars + 56, ds_free = bars + 64;
-  const uint32_t dq_full = bars + 72, dq_free = bars + 80, acc_full = bars + 88;
-  const uint32_t tmem_slot = bars + 96;
-  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SM_BAR + 96);
+  auto ld_empty = [&](int s) { return bars + 8 + 8 * NST + 8 * s; };
+  const uint32_t b0 = bars + 8 + 16 * NST;
+  const uint32_t s_full = b0, dp_free = b0 + 8, p_full = b0 + 16;
+  auto ds_free = [&](int b) { return b0 + 24 + 8 * b; };
+  const uint32_t dq_full = b0 + 40, dq_free = b0 + 48, acc_full = b0 + 56;
+  const uint32_t tmem_slot = b0 + 64;
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SM_BAR + 8 + 16 * NST + 64);
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -132,14 +138,15 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     tma_prefetch_desc(&tmDO);
     tma_prefetch_desc(&tmDQ);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(ld_full(s), 1);
       mbar_init(ld_empty(s), 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(dp_free, 4);
-    mbar_init(p_full, 4);
-    mbar_init(ds_free, 1);
+    mbar_init(dp_free, 8);
+    mbar_init(p_full, 8);
+    mbar_init(ds_free(0), 1);
+    mbar_init(ds_free(1), 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(acc_full, 1);
@@ -161,9 +168,9 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       }
       const size_t row0 = (size_t)bh * p.nq * BQ;
       for (int t = 0; t < n; ++t) {
-        const int s = t & 1;
+        const int s = t % NST;
         const int i = i_lo + t;
-        mbar_wait(ld_empty(s), ((t >> 1) & 1) ^ 1, 1);
+        mbar_wait(ld_empty(s), ((t / NST) & 1) ^ 1, 1);
         mbar_arrive_expect_tx(ld_full(s), 2 * QT_BYTES + 512);
         for (int h = 0; h < 2; ++h) {
           tma_load_3d(sbase + SM_Q + s * QT_BYTES + h * QPANEL, &tmQ, ld_full(s), 64 * h, i * BQ, bh);
@@ -180,12 +187,12 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       constexpr uint32_t HI = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, version 1, SW128
       constexpr uint32_t LO_K = (16u >> 4) << 16;                       // K-major: LBO unused
       auto issue_S = [&](int t, bool dp) {
-        const int s = t & 1;
-        if (!dp) mbar_wait(ld_full(s), (t >> 1) & 1, 2);
+        const int st = t % NST;
+        if (!dp) mbar_wait(ld_full(st), (t / NST) & 1, 2);
         tc_fence_after();
         const uint32_t a0 = (sbase + (dp ? SM_V : SM_K)) >> 4;
-        const uint32_t b0 = (sbase + (dp ? SM_DO : SM_Q) + s * QT_BYTES) >> 4;
-        const uint32_t d = tm + (dp ? TM_DP : TM_S + 64 * s);
+        const uint32_t b0 = (sbase + (dp ? SM_DO : SM_Q) + st * QT_BYTES) >> 4;
+        const uint32_t d = tm + (dp ? TM_DP : TM_S + 64 * (t & 1));
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
@@ -204,7 +211,8 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       __syncwarp();
       if (n > 1) issue_S(1, false);
       for (int t = 0; t < n; ++t) {
-        const int s = t & 1;
+        const int s = t & 1;      // S^T buffer and dS^T smem buffer
+        const int st = t % NST;   // Q / dO stage
         if (t + 1 < n) {
           mbar_wait(dp_free, t & 1, 4);  // dP^T_t is in the softmax warps' registers
           issue_S(t + 1, true);
@@ -218,20 +226,21 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           tc_fence_after();
         }
         if (elect_one()) {
-          const uint32_t bq = (sbase + SM_Q + s * QT_BYTES) >> 4;
-          const uint32_t bdo = (sbase + SM_DO + s * QT_BYTES) >> 4;
+          const uint32_t bq = (sbase + SM_Q + st * QT_BYTES) >> 4;
+          const uint32_t bdo = (sbase + SM_DO + st * QT_BYTES) >> 4;
           constexpr uint32_t LO_QMN = ((uint32_t)QPANEL >> 4) << 16;  // LBO: D-panel stride
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k) {  // K = 64 queries: 16 query rows (2 KiB) per step
-            const uint32_t a_p = tm + TM_S + 64 * s + k * 8;
-            const uint32_t a_ds = tm + TM_S + 64 * s + 32 + k * 8;
+            // query half h = k / 2 lives in columns [32h, 32h + 32): P^T | dS^T
+            const uint32_t a_p = tm + TM_S + 64 * s + 32 * (k >> 1) + 8 * (k & 1);
+            const uint32_t a_ds = a_p + 16;
             mma_f16_ts<1>(tm + TM_DV, a_p, make_desc(LO_QMN | (bdo + k * (2048 >> 4)), HI), IDESC_KV,
                           (t | k) != 0);
             mma_f16_ts<1>(tm + TM_DK, a_ds, make_desc(LO_QMN | (bq + k * (2048 >> 4)), HI), IDESC_KV,
                           (t | k) != 0);
           }
           const uint32_t ak = (sbase + SM_K) >> 4;
-          const uint32_t bds = (sbase + SM_DS) >> 4;
+          const uint32_t bds = (sbase + SM_DS + s * BKV * 128) >> 4;
           constexpr uint32_t LO_KMN = ((uint32_t)KPANEL >> 4) << 16;  // LBO: D-panel stride of K
           constexpr uint32_t LO_DSMN = ((uint32_t)(BKV * 128) >> 4) << 16;
 #pragma unroll
@@ -239,17 +248,18 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             mma_f16_ss<1>(tm + TM_DQ, make_desc(LO_KMN | (ak + k * (2048 >> 4)), HI),
                           make_desc(LO_DSMN | (bds + k * (2048 >> 4)), HI), IDESC_DQ, k != 0);
           mma_commit(dq_full);
-          mma_commit(ld_empty(s));
-          mma_commit(ds_free);
+          mma_commit(ld_empty(st));
+          mma_commit(ds_free(s));
           if (t == n - 1) mma_commit(acc_full);
         }
         __syncwarp();
         if (t + 2 < n) issue_S(t + 2, false);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ================= softmax warpgroup (lane = key) =================
+  } else if (warp >= 4 && warp < 12) {
+    // ================= softmax warpgroups (lane = key, ch = query half) =================
     const int qq = warp & 3;
+    const int ch = (warp - 4) >> 2;
     const int krow = qq * 32 + (int)lane;      // key row inside the tile
     const int key = j * BKV + krow;
     const uint32_t t_lane = (uint32_t)(qq * 32) << 16;
@@ -258,24 +268,22 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       const int i = i_lo + t;
       mbar_wait(s_full, t & 1, 7);
       tc_fence_after();
-      uint32_t sv[64], dp[64];
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 64 * s, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 64 * s + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_DP, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_DP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dp[32]));
+      uint32_t sv[32], dp[32];
+      const uint32_t t_s = tmem + t_lane + TM_S + 64 * s + 32 * ch;
+      tmem_ld_32x32b_x32(t_s, sv);
+      tmem_ld_32x32b_x32(tmem + t_lane + TM_DP + 32 * ch, dp);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dp_free);
-      // lse2 / D of the 64 queries (the ld_full wait of the MMA warp already
-      // covers them; wait here too: this warp reads them itself)
-      mbar_wait(ld_full(s), (t >> 1) & 1, 8);
-      const float *lse2 = reinterpret_cast<const float *>(smem + SM_LD + s * 512);
+      // lse2 / D of this half's 32 queries (the stage's ld_full also covers them)
+      mbar_wait(ld_full(t % NST), (t / NST) & 1, 8);
+      const float *lse2 = reinterpret_cast<const float *>(smem + SM_LD + (t % NST) * 512) + 32 * ch;
       const float *dv = lse2 + 64;
-      const int q0 = i * BQ;
-      uint32_t pk[32], dk2[32];
+      const int q0 = i * BQ + 32 * ch;
+      uint32_t pk[16], dk2[16];
 #pragma unroll
-      for (int c4 = 0; c4 < 16; ++c4) {
+      for (int c4 = 0; c4 < 8; ++c4) {
         const float4 l4 = *reinterpret_cast<const float4 *>(lse2 + 4 * c4);
         const float4 d4 = *reinterpret_cast<const float4 *>(dv + 4 * c4);
         const float la[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -296,18 +304,17 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         dk2[2 * c4] = pack_bf16(dsv[0], dsv[1]);
         dk2[2 * c4 + 1] = pack_bf16(dsv[2], dsv[3]);
       }
-      // P^T / dS^T (bf16) over the S^T columns this thread has already read
-      tmem_st_32x32b_x16(tmem + t_lane + TM_S + 64 * s, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      tmem_st_32x32b_x16(tmem + t_lane + TM_S + 64 * s + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
-      tmem_st_32x32b_x16(tmem + t_lane + TM_S + 64 * s + 32, *reinterpret_cast<uint32_t(*)[16]>(&dk2[0]));
-      tmem_st_32x32b_x16(tmem + t_lane + TM_S + 64 * s + 48, *reinterpret_cast<uint32_t(*)[16]>(&dk2[16]));
-      // dS^T row -> smem (B operand of dQ^T, MN-major SW128: 16-B chunk c of row r at c ^ (r & 7))
-      if (t >= 1) mbar_wait(ds_free, (t - 1) & 1, 9);
-      const uint32_t rbase = sbase + SM_DS + krow * 128;
+      // P^T | dS^T (bf16) over this half's S^T columns, already read
+      tmem_st_32x32b_x16(t_s, pk);
+      tmem_st_32x32b_x16(t_s + 16, dk2);
+      // dS^T half-row -> smem buffer s (B operand of dQ^T, MN-major SW128:
+      // 16-B chunk c of row r at c ^ (r & 7)); buffer s was last read by dQ_{t-2}
+      if (t >= 2) mbar_wait(ds_free(s), ((t - 2) >> 1) & 1, 9);
+      const uint32_t rbase = sbase + SM_DS + s * BKV * 128 + krow * 128;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        st_shared_v4(rbase + ((c ^ (krow & 7)) * 16), dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2],
-                     dk2[4 * c + 3]);
+      for (int c = 0; c < 4; ++c)
+        st_shared_v4(rbase + (((4 * ch + c) ^ (krow & 7)) * 16), dk2[4 * c], dk2[4 * c + 1],
+                     dk2[4 * c + 2], dk2[4 * c + 3]);
       fence_async_smem();
       tmem_st_wait();
       tc_fence_before();
@@ -319,7 +326,8 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       mbar_wait(acc_full, 0, 10);
       tc_fence_after();
     }
-    for (int which = 0; which < 2; ++which) {
+    {
+      const int which = ch;  // warpgroup 0 writes dV, warpgroup 1 dK
       __nv_bfloat16 *dst = which == 0 ? p.dv : p.dk;
       const float mul = which == 0 ? 1.f : p.scale;
       uint4 *orow = reinterpret_cast<uint4 *>(dst + ((size_t)bh * p.seq + key) * D);
@@ -346,7 +354,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ================= dQ drain (lane = head-dim row of dQ^T) =================
     const int dd = warp & 3;
     const uint32_t t_lane = (uint32_t)(dd * 32) << 16;

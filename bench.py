@@ -620,6 +620,59 @@ def bench_simplicial(args, rank, ws, local):
             "clocks": clocks}
 
 
+BWD_B, BWD_H, BWD_S = 4, 48, 8192  # PAPER.md:713 ABC4 (backward, non-causal, D=128)
+
+
+def bench_attention_bwd(args, rank, ws, local):
+    """attention backward, PAPER.md:713 ABC4 (B=4 H=48
+    S=8192 D=128, non-causal), heads split across ranks; the non-causal
+    forward (AFN4) timed on the same inputs.  FLOP: forward 4*S^2*D per head,
+    backward 2.5x that (five S^2*D GEMMs)."""
+    import torch
+    import paper_2605_10905_b200 as P
+    from paper_2605_10905_b200 import shard
+    pk = peaks()
+    dev = torch.device("cuda", local)
+    r0, r1 = shard.head_shards(BWD_B * BWD_H, ws)[rank]
+    bh = max(1, r1 - r0)
+    g = torch.Generator(device=dev).manual_seed(13 + rank)
+    q, k, v, do = ((torch.rand((1, bh, BWD_S, 128), device=dev, generator=g) * 2 - 1).bfloat16()
+                   for _ in range(4))
+    o, lse = P.attention_fwd(q, k, v, causal=False)
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    stream = torch.cuda.current_stream()
+
+    def fwd():
+        P.attention_fwd(q, k, v, causal=False, out=o, lse=lse)
+
+    def bwd():
+        P.attention_bwd(q, k, v, o, do, lse, causal=False, dq=dq, dk=dk, dv=dv)
+
+    steps = max(3, args.steps // 10)
+    fsecs = timed(fwd, steps, args.warmup, ws, stream)
+    clk = Clocks(local)
+    clk.start()
+    secs = timed(bwd, steps, args.warmup, ws, stream)
+    clocks = clk.stop()
+    fwd_flop_head = 4.0 * BWD_S * BWD_S * 128
+    per = secs / steps
+    achieved = 2.5 * fwd_flop_head * (r1 - r0) / per / 1e12
+    return {"value": round(2.5 * fwd_flop_head * BWD_B * BWD_H * steps / secs / 1e12, 1),
+            "unit": "TFLOPS", "ms_per_step": round(per * 1e3, 4), "scaling": "strong",
+            "config": {"workload": "attention backward (SURVEY §8f rank 4), PAPER.md:713 ABC4 "
+                                   "B=4 H=48 S=8192 D=128 non-causal, bf16, dQ by TMA reduce-add",
+                       "l2": "Q, K, V, O, dO 5 x 384 MiB > L2"},
+            "noncausal_fwd": {"value": round(fwd_flop_head * BWD_B * BWD_H * steps / fsecs / 1e12, 1),
+                              "unit": "TFLOPS", "ms_per_step": round(fsecs / steps * 1e3, 4),
+                              "workload": "PAPER.md:708 AFN4 B=4 H=48 S=8192 D=128 non-causal"},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk["bf16"],
+                         "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
+                         "peak_source": f"{pk['src']} bf16 burst",
+                         "algorithmic_flop_per_launch": 2.5 * fwd_flop_head * (r1 - r0),
+                         "traffic": traffic("attention_bwd")},
+            "clocks": clocks}
+
+
 MD_SHAPE = ("GD1", 8192, 2048, 16384)  # PAPER.md:751 multi-GPU GEMM shape (M, N, K)
 NVLINK_GBS = 770.0  # B200_PROFILING.md: measured peer copy bandwidth per direction
 
@@ -725,7 +778,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm", "simplicial",
-                             "multidevice"])
+                             "multidevice", "attention_bwd"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -773,6 +826,8 @@ def main():
         res = bench_simplicial(args, rank, ws, local)
     elif args.workload == "multidevice":
         res = bench_multidevice(args, rank, ws, local)
+    elif args.workload == "attention_bwd":
+        res = bench_attention_bwd(args, rank, ws, local)
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
@@ -789,6 +844,9 @@ def main():
             torch_empty_cache()
             res["secondary"]["layernorm_cluster"] = bench_layernorm(args, rank, ws, local)
             res["secondary"]["simplicial_attention"] = bench_simplicial(args, rank, ws, local)
+            torch_empty_cache()
+            res["secondary"]["attention_bwd"] = bench_attention_bwd(args, rank, ws, local)
+            torch_empty_cache()
             try:
                 if ws > 1 and not os.environ.get("MIMW_BENCH_MD"):
                     # real peers need every rank's kernel in the device barrier: opt-in

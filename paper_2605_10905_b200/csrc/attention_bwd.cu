@@ -125,11 +125,18 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
-  const int j = blockIdx.x / p.bh;   // KV tile (ascending: the longest causal items first)
-  const int bh = blockIdx.x % p.bh;
+  // Head-major order: the KV tiles of one head run together, so the head's
+  // Q / dO (read by every one of them) and its dQ accumulator (reduced into by
+  // every one of them) stay L2-resident.  Measured with the KV-tile-major
+  // order: 157 GB of DRAM traffic per ABC4 launch (dQ reductions missing L2).
+  const int bh = blockIdx.x / p.nkv;
+  const int j = blockIdx.x % p.nkv;
   int i_lo, i_hi;
   q_range(j, p, i_lo, i_hi);
   const int n = i_hi - i_lo + 1;
+  // step t visits query tile i_lo + (t + j) % n: the head's KV tiles start at
+  // different query tiles, so their dQ reductions do not pile onto one tile
+  auto q_tile = [&](int t) { int r = t + j; r -= (r / n) * n; return i_lo + r; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -169,7 +176,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       const size_t row0 = (size_t)bh * p.nq * BQ;
       for (int t = 0; t < n; ++t) {
         const int s = t % NST;
-        const int i = i_lo + t;
+        const int i = q_tile(t);
         mbar_wait(ld_empty(s), ((t / NST) & 1) ^ 1, 1);
         mbar_arrive_expect_tx(ld_full(s), 2 * QT_BYTES + 512);
         for (int h = 0; h < 2; ++h) {
@@ -265,7 +272,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     const uint32_t t_lane = (uint32_t)(qq * 32) << 16;
     for (int t = 0; t < n; ++t) {
       const int s = t & 1;
-      const int i = i_lo + t;
+      const int i = q_tile(t);
       mbar_wait(s_full, t & 1, 7);
       tc_fence_after();
       uint32_t sv[32], dp[32];
@@ -360,7 +367,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     const uint32_t t_lane = (uint32_t)(dd * 32) << 16;
     const uint32_t stage = sbase + SM_DQ + dd * 8192;
     for (int t = 0; t < n; ++t) {
-      const int i = i_lo + t;
+      const int i = q_tile(t);
       mbar_wait(dq_full, t & 1, 11);
       tc_fence_after();
       uint32_t v[64];

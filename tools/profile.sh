@@ -31,6 +31,18 @@ for what in "$@"; do
       timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
         -k regex:GroupedSched -s 3 -c 1 -o "$OUT/moe" -f \
         python bench.py --workload moe --steps 1 --warmup 3 --no-cpu > "$OUT/moe_ncu.log" 2>&1 ;;
+    md)
+      timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
+        -k regex:GatherSched -s 3 -c 1 -o "$OUT/md" -f \
+        python bench.py --workload multidevice --steps 2 --warmup 3 --no-cpu > "$OUT/md_ncu.log" 2>&1 ;;
+    bwd)
+      timeout 900 $NCU --set full --import-source on -k regex:attention_bwd_kernel -s 1 -c 1 \
+        -o "$OUT/bwd" -f python bench.py --workload attention_bwd --steps 3 --warmup 3 --no-cpu \
+        > "$OUT/bwd_ncu.log" 2>&1 ;;
+    simp)
+      timeout 900 $NCU --set full --import-source on -k regex:simplicial -s 1 -c 1 \
+        -o "$OUT/simp" -f python bench.py --workload simplicial --steps 3 --warmup 3 --no-cpu \
+        > "$OUT/simp_ncu.log" 2>&1 ;;
   esac
   echo "$what rc=$?"
 done

@@ -20,12 +20,17 @@
 //
 // MIMW roles (one CTA = 128 query rows of one (batch, head), 6 warps):
 //   warp 0     TMA producer of the K2/V2 tile ring (repeated for every d)
-//   warp 1     TMEM allocator + single-thread MMA issuer; S(step n) is issued
-//              before PV(step n-1) so the next S overlaps the softmax
+//   warp 1     TMEM allocator + single-thread MMA issuer, running two S tiles
+//              ahead: S(n+2) is issued right after PV(n) (tcgen05.mma ops of
+//              one thread execute in order, so it may overwrite P_n)
 //   warps 2-5  Q' preparation, softmax, U -> O fold, epilogue (1 row/thread)
-// TMEM: S [0,128) f32, P [128,192) bf16, U [256,384) f32, O [384,512) f32.
+// TMEM: S double buffer [0,128) [128,256) f32 (P_n bf16 written over the first
+// 64 columns of its own S buffer once read), U [256,384) f32, O [384,512) f32.
+// The softmax warps wait on a PV only to rescale (the running max grew) or to
+// fold U_d into O; otherwise the tensor pipe always holds the next S.
 #include "simplicial_fwd.h"
 #include "ptx.cuh"
+#include "softmax.cuh"
 #include "tma_host.h"
 
 #include <algorithm>
@@ -47,7 +52,7 @@ constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_U = 256, TM_O = 384;
+constexpr uint32_t TM_S = 0, TM_U = 256, TM_O = 384;  // S buffer b at TM_S + 128 b
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct Params {
@@ -56,19 +61,8 @@ struct Params {
   float *lse;
   int seq, w1, w2, nqt;
   float scale_log2;
+  int scale_pos;     // scale > 0: max on raw scores, scale folded into the FFMA2
 };
-
-__device__ __forceinline__ uint64_t make_desc(uint32_t lo, uint32_t hi) {
-  uint64_t r;
-  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
-  return r;
-}
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // K2/V2 tile range [lo, hi] needed by query rows [i0, i0+127]
 __device__ __forceinline__ void kv2_range(int i0, const Params &p, int &lo, int &hi) {
@@ -85,11 +79,16 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
   const uint32_t bars = sbase + SMEM_BAR;
   auto qp_full = [&](int b) { return bars + 8 * b; };
   auto qp_empty = [&](int b) { return bars + 16 + 8 * b; };
-  const uint32_t s_full = bars + 32, s_free = bars + 40, p_full = bars + 48, u_done = bars + 56;
-  auto kv_full = [&](int s) { return bars + 64 + 8 * s; };
-  auto kv_empty = [&](int s) { return bars + 64 + 8 * NSLOT + 8 * s; };
-  const uint32_t tmem_slot = bars + 64 + 16 * NSLOT;
-  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 64 + 16 * NSLOT);
+  auto s_full = [&](int b) { return bars + 32 + 8 * b; };
+  // Step n uses p_full(n & 1) / u_done(n & 1): the softmax warps run up to
+  // two steps ahead of the MMA warp's P waits and wait on a PV up to two steps
+  // late, which a single parity-tracked barrier could not disambiguate.
+  auto p_full = [&](int b) { return bars + 48 + 8 * b; };
+  auto u_done = [&](int b) { return bars + 64 + 8 * b; };
+  auto kv_full = [&](int s) { return bars + 80 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 80 + 8 * NSLOT + 8 * s; };
+  const uint32_t tmem_slot = bars + 80 + 16 * NSLOT;
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 80 + 16 * NSLOT);
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -109,10 +108,12 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       mbar_init(qp_full(b), 4);
       mbar_init(qp_empty(b), 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 4);
-    mbar_init(p_full, 4);
-    mbar_init(u_done, 1);
+    mbar_init(s_full(0), 1);
+    mbar_init(s_full(1), 1);
+    mbar_init(p_full(0), 4);
+    mbar_init(p_full(1), 4);
+    mbar_init(u_done(0), 1);
+    mbar_init(u_done(1), 1);
     for (int s = 0; s < NSLOT; ++s) {
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
@@ -149,15 +150,12 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);
     constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;
     constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;
-    uint32_t sf_phase = 0, pf_phase = 0;
     auto ring_wait = [&](int pos) { mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71); };
-    auto issue_S = [&](int n) {  // S of step n = (d, t)
+    auto issue_S = [&](int n) {  // S of step n = (d, t) into buffer n & 1
       const int d = n / ntile;
       const int t = n % ntile;
       if (t == 0) mbar_wait(qp_full(d & 1), (d >> 1) & 1, 72);
       ring_wait(2 * n);
-      mbar_wait(s_free, sf_phase ^ 1, 73);
-      sf_phase ^= 1;
       tc_fence_after();
       const uint32_t qa = (sbase + SMEM_QP + (d & 1) * TILE_BYTES) >> 4;
       const uint32_t kb = (sbase + SMEM_KV + ((2 * n) % NSLOT) * TILE_BYTES) >> 4;
@@ -165,10 +163,10 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = ((k >> 2) * HALF_BYTES + (k & 3) * 32) >> 4;
-          mma_f16_ss<1>(tmem + TM_S, make_desc(LO_KMAJ | (qa + off), HI_KMAJ),
+          mma_f16_ss<1>(tmem + TM_S + 128 * (n & 1), make_desc(LO_KMAJ | (qa + off), HI_KMAJ),
                         make_desc(LO_KMAJ | (kb + off), HI_KMAJ), IDESC_S, k != 0);
         }
-        mma_commit(s_full);
+        mma_commit(s_full(n & 1));
         mma_commit(kv_empty((2 * n) % NSLOT));
         if (t == ntile - 1) mma_commit(qp_empty(d & 1));  // last read of Q'_d
       }
@@ -177,24 +175,25 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     auto issue_PV = [&](int n) {
       const int t = n % ntile;
       ring_wait(2 * n + 1);
-      mbar_wait(p_full, pf_phase, 74);
-      pf_phase ^= 1;
+      mbar_wait(p_full(n & 1), (uint32_t)((n >> 1) & 1), 74);
       tc_fence_after();
       const uint32_t vb = (sbase + SMEM_KV + ((2 * n + 1) % NSLOT) * TILE_BYTES) >> 4;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          mma_f16_ts<1>(tmem + TM_U, tmem + TM_P + k * 8,
+          mma_f16_ts<1>(tmem + TM_U, tmem + TM_S + 128 * (n & 1) + k * 8,
                         make_desc(LO_VMN | (vb + k * (2048 >> 4)), HI_KMAJ), IDESC_PV,
                         (t != 0 || k != 0) ? 1u : 0u);
-        mma_commit(u_done);
+        mma_commit(u_done(n & 1));
         mma_commit(kv_empty((2 * n + 1) % NSLOT));
       }
       __syncwarp();
     };
-    for (int n = 0; n <= nsteps; ++n) {
-      if (n < nsteps) issue_S(n);
-      if (n > 0) issue_PV(n - 1);
+    if (nsteps > 0) issue_S(0);
+    if (nsteps > 1) issue_S(1);
+    for (int n = 0; n < nsteps; ++n) {
+      issue_PV(n);
+      if (n + 2 < nsteps) issue_S(n + 2);  // overwrites P_n: after PV(n) in issue order
     }
   } else {
     // ================= Q' prep / softmax / U->O fold / epilogue =================
@@ -205,13 +204,8 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     const bool row_live = i < p.seq;
     const __nv_bfloat16 *qrow = p.q + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D;
     float m_used = -INFINITY, l = 0.f;
-    uint32_t s_phase = 0;
-    int pv_seen = 0;  // PV steps known complete (u_done phases consumed)
     auto wait_pv = [&](int k) {  // PV of step k complete
-      while (pv_seen <= k) {
-        mbar_wait(u_done, (uint32_t)(pv_seen & 1), 77);
-        ++pv_seen;
-      }
+      mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77);
       tc_fence_after();
     };
     bool o_live = false;  // O holds a folded U
@@ -246,38 +240,49 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(qp_full(d & 1));
     };
-    const float sl = p.scale_log2;
+    const float sl = p.scale_pos ? p.scale_log2 : 1.f;
+    const uint64_t sl2 = f2_pack(sl, sl);
+    prep_qp(0);
     for (int n = 0; n < nsteps; ++n) {
       const int d = n / ntile;
       const int t = n % ntile;
       const int j1 = i - d;
-      if (n == 0) prep_qp(0);
+      const int b = n & 1;
       // ---- S of step n ----
-      mbar_wait(s_full, s_phase, 76);
-      s_phase ^= 1;
+      mbar_wait(s_full(b), (uint32_t)((n >> 1) & 1), 76);
       tc_fence_after();
       uint32_t s[128];
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-      tmem_ld_32x32b_x32(tmem + t_lane + TM_S + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+      const uint32_t t_s = tmem + t_lane + TM_S + 128 * b;
+      tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      tmem_ld_32x32b_x32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+      tmem_ld_32x32b_x32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);
-      // mask: j2 in [i - w2 + 1, i], valid query row, valid K1 row
+      // mask: j2 in [i - w2 + 1, i] and < seq, valid query row, valid K1 row.
+      // Uniform fast path: the tile is inside every row's window.
       const int k0 = (lo + t) * BKV;
-      const int c_lo = i - p.w2 + 1 - k0;
-      const int c_hi = min(i, p.seq - 1) - k0;
+      const bool need_mask = (k0 + BKV - 1 > i0) || (k0 < i0 + BQ - p.w2) || (k0 + BKV > p.seq) ||
+                             (i0 + BQ > p.seq) || (i0 < d) || !p.scale_pos;
       const bool live = row_live && j1 >= 0;
-      float mx = -INFINITY;
+      if (need_mask) {
+        const int c_lo = i - p.w2 + 1 - k0;
+        const int c_hi = min(i, p.seq - 1) - k0;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        float v = __uint_as_float(s[c]) * sl;
-        if (!live || c < c_lo || c > c_hi) v = -INFINITY;
-        s[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        for (int c = 0; c < 128; ++c) {
+          float v = __uint_as_float(s[c]);
+          if (!p.scale_pos) v *= p.scale_log2;
+          if (!live || c < c_lo || c > c_hi) v = -INFINITY;
+          s[c] = __float_as_uint(v);
+        }
       }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 128; c += 8) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
+      }
+      const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
@@ -286,21 +291,28 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
         m_used = mx;
       }
       l *= corr;
-      const float nm = (m_used == -INFINITY) ? 0.f : m_used;
+      const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
+      const uint64_t nm2 = f2_pack(nm, nm);
+      uint64_t acc2[4] = {0, 0, 0, 0};
       uint32_t pk[64];
-      float acc = 0.f;
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
-        const float p0 = ex2(__uint_as_float(s[2 * e]) - nm);
-        const float p1 = ex2(__uint_as_float(s[2 * e + 1]) - nm);
-        acc += p0 + p1;
-        pk[e] = pack_bf16(p0, p1);
+        const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), sl2, nm2);
+        const uint64_t p2 = ex2_mufu2(x2);
+        acc2[e & 3] = f2_add(acc2[e & 3], p2);
+        pk[e] = pack_bf16_2(p2);
       }
-      l += acc;
-      // PV of the previous step must be done before P / U / O are touched
-      if (n > 0) wait_pv(n - 1);
+      {
+        float a0, a1, b0, b1;
+        f2_unpack(f2_add(acc2[0], acc2[1]), a0, a1);
+        f2_unpack(f2_add(acc2[2], acc2[3]), b0, b1);
+        l += (a0 + a1) + (b0 + b1);
+      }
+      // P_n overwrites S buffer b, last read as P_{n-2} by PV(n-2)
+      if (n >= 2) wait_pv(n - 2);
       if (__any_sync(0xffffffffu, rescale)) {
         // U (this d's partial sum, if any PV of it ran) and O carry the old max
+        if (n >= 1) wait_pv(n - 1);
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t o[32];
@@ -324,14 +336,14 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       }
 #pragma unroll
       for (int c = 0; c < 64; c += 16)
-        tmem_st_32x32b_x16(tmem + t_lane + TM_P + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
+        tmem_st_32x32b_x16(t_s + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(p_full(b));
+      // next d's Q' early: the MMA warp runs two S tiles ahead
+      if (t == 0 && d + 1 < nd) prep_qp(d + 1);
       if (t == ntile - 1) {
-        // next d's Q' first: its S may enter the pipe while this d is folded
-        if (d + 1 < nd) prep_qp(d + 1);
         // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
         wait_pv(n);
         const uint4 *vv = reinterpret_cast<const uint4 *>(p.v1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
@@ -418,6 +430,7 @@ cudaError_t simplicial_fwd_launch(const SimplicialArgs &a, cudaStream_t stream) 
   p.w2 = (int)std::min<int64_t>(a.w2, a.seq);
   p.nqt = (int)((a.seq + BQ - 1) / BQ);
   p.scale_log2 = (float)(a.scale * 1.4426950408889634);
+  p.scale_pos = a.scale > 0 ? 1 : 0;
   cudaError_t e = cudaFuncSetAttribute(simplicial_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        SMEM_TOTAL);
   if (e != cudaSuccess) return e;

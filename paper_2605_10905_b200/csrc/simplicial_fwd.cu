@@ -18,12 +18,16 @@
 // with ONE running max / sum per row across all (d, j2), so O and U are
 // rescaled together (only when the max grows by > 8 in log2 units).
 //
-// MIMW roles (one CTA = 128 query rows of one (batch, head), 6 warps):
+// MIMW roles (one CTA = 128 query rows of one (batch, head), 8 warps):
 //   warp 0     TMA producer of the K2/V2 tile ring (repeated for every d)
 //   warp 1     TMEM allocator + single-thread MMA issuer, running two S tiles
 //              ahead: S(n+2) is issued right after PV(n) (tcgen05.mma ops of
 //              one thread execute in order, so it may overwrite P_n)
-//   warps 2-5  Q' preparation, softmax, U -> O fold, epilogue (1 row/thread)
+//   warps 2-5  softmax, U -> O fold, epilogue (1 row/thread)
+//   warps 6-7  operand prep (2 rows/thread): Q'_{d+1} = q (.) k1[i-d-1] into
+//              the Q' double buffer and the v1[i-d] rows of the fold into smem,
+//              off the softmax warps' critical path (their global-load latency
+//              was ~25% of the kernel, measured)
 // TMEM: S double buffer [0,128) [128,256) f32 (P_n bf16 written over the first
 // 64 columns of its own S buffer once read), U [256,384) f32, O [384,512) f32.
 // The softmax warps wait on a PV only to rescale (the running max grew) or to
@@ -45,10 +49,11 @@ constexpr int BKV = 128;
 constexpr int NSLOT = 4;
 constexpr int TILE_BYTES = BKV * D * 2;     // 32 KiB
 constexpr int HALF_BYTES = TILE_BYTES / 2;  // one 64-column swizzle panel
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 256;
 constexpr int SMEM_QP = 0;                               // 2 Q' buffers
 constexpr int SMEM_KV = 2 * TILE_BYTES;                  // K2/V2 ring
-constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
+constexpr int SMEM_V1 = SMEM_KV + NSLOT * TILE_BYTES;     // v1[i - d] rows of the fold
+constexpr int SMEM_BAR = SMEM_V1 + TILE_BYTES;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);
@@ -87,8 +92,9 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
   auto u_done = [&](int b) { return bars + 64 + 8 * b; };
   auto kv_full = [&](int s) { return bars + 80 + 8 * s; };
   auto kv_empty = [&](int s) { return bars + 80 + 8 * NSLOT + 8 * s; };
-  const uint32_t tmem_slot = bars + 80 + 16 * NSLOT;
-  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 80 + 16 * NSLOT);
+  const uint32_t v1_full = bars + 80 + 16 * NSLOT, v1_empty = v1_full + 8;
+  const uint32_t tmem_slot = v1_full + 16;
+  volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 96 + 16 * NSLOT);
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -105,7 +111,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     tma_prefetch_desc(&tmK2);
     tma_prefetch_desc(&tmV2);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(qp_full(b), 4);
+      mbar_init(qp_full(b), 2);  // the two prep warps
       mbar_init(qp_empty(b), 1);
     }
     mbar_init(s_full(0), 1);
@@ -118,6 +124,8 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
     }
+    mbar_init(v1_full, 2);
+    mbar_init(v1_empty, 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
@@ -195,27 +203,21 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       issue_PV(n);
       if (n + 2 < nsteps) issue_S(n + 2);  // overwrites P_n: after PV(n) in issue order
     }
-  } else {
-    // ================= Q' prep / softmax / U->O fold / epilogue =================
-    const int q = warp & 3;
-    const int row = q * 32 + (int)lane;  // row of the tile == TMEM lane
-    const int i = i0 + row;
-    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const bool row_live = i < p.seq;
-    const __nv_bfloat16 *qrow = p.q + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D;
-    float m_used = -INFINITY, l = 0.f;
-    auto wait_pv = [&](int k) {  // PV of step k complete
-      mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77);
-      tc_fence_after();
-    };
-    bool o_live = false;  // O holds a folded U
+  } else if (warp >= 6) {
+    // ================= operand prep: Q'_d and v1 rows (rows r, r + 32) =================
+    const int pw0 = (warp - 6) * 64 + (int)lane;
     // ---- Q'_d = q (.) k1[i - d] into smem buffer d&1 (SW128 K-major) ----
     auto prep_qp = [&](int d) {
-      const int j1 = i - d;
       if (d >= 2) mbar_wait(qp_empty(d & 1), ((d >> 1) & 1) ^ 1, 75);
       const uint32_t buf = sbase + SMEM_QP + (d & 1) * TILE_BYTES;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+      const int row = pw0 + 32 * h;
+      const int i = i0 + row;
+      const bool row_live = i < p.seq;
+      const uint4 *qv = reinterpret_cast<const uint4 *>(p.q + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D);
+      const int j1 = i - d;
       const bool ok = row_live && j1 >= 0;
-      const uint4 *qv = reinterpret_cast<const uint4 *>(qrow);
       const uint4 *kv = reinterpret_cast<const uint4 *>(p.k1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
 #pragma unroll 4
       for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 bf16
@@ -236,13 +238,51 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
                          ((cc ^ (row & 7)) << 4),
                      w.x, w.y, w.z, w.w);
       }
+      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(qp_full(d & 1));
     };
+    // ---- v1[i - d] row for the fold of d: 16-B chunk c of row r at c ^ (r & 15) ----
+    auto prep_v1 = [&](int d) {
+      if (d >= 1) mbar_wait(v1_empty, (uint32_t)((d - 1) & 1), 78);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int row = pw0 + 32 * h;
+        const int i = i0 + row;
+        const int j1 = i - d;
+        const bool ok = i < p.seq && j1 >= 0;
+        const uint4 *vv = reinterpret_cast<const uint4 *>(p.v1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
+        uint4 w[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) w[c] = ok ? __ldg(vv + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          st_shared_v4(sbase + SMEM_V1 + row * 256 + ((c ^ (row & 15)) << 4), w[c].x, w[c].y, w[c].z, w[c].w);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v1_full);
+    };
+    if (nd > 0) prep_qp(0);
+    for (int d = 0; d < nd; ++d) {
+      if (d + 1 < nd) prep_qp(d + 1);
+      prep_v1(d);
+    }
+  } else if (warp >= 2) {
+    // ================= softmax / U->O fold / epilogue =================
+    const int q = warp & 3;
+    const int row = q * 32 + (int)lane;  // row of the tile == TMEM lane
+    const int i = i0 + row;
+    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+    const bool row_live = i < p.seq;
+    float m_used = -INFINITY, l = 0.f;
+    auto wait_pv = [&](int k) {  // PV of step k complete
+      mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77);
+      tc_fence_after();
+    };
+    bool o_live = false;  // O holds a folded U
     const float sl = p.scale_pos ? p.scale_log2 : 1.f;
     const uint64_t sl2 = f2_pack(sl, sl);
-    prep_qp(0);
     for (int n = 0; n < nsteps; ++n) {
       const int d = n / ntile;
       const int t = n % ntile;
@@ -341,12 +381,10 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full(b));
-      // next d's Q' early: the MMA warp runs two S tiles ahead
-      if (t == 0 && d + 1 < nd) prep_qp(d + 1);
       if (t == ntile - 1) {
         // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
         wait_pv(n);
-        const uint4 *vv = reinterpret_cast<const uint4 *>(p.v1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
+        mbar_wait(v1_full, (uint32_t)(d & 1), 79);
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t u[32], o[32];
@@ -355,8 +393,11 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
           tmem_ld_wait();
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            uint4 w = make_uint4(0, 0, 0, 0);
-            if (live) w = __ldg(vv + c / 8 + g);
+            uint4 w;
+            const int ch = c / 8 + g;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(sbase + SMEM_V1 + row * 256 + ((ch ^ (row & 15)) << 4)));
             const uint32_t *pw = &w.x;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -372,6 +413,8 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
           tmem_st_32x32b_x16(tmem + t_lane + TM_O + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
         }
         tmem_st_wait();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(v1_empty);  // v1 rows of d read
         o_live = true;
         // the PV issuer overwrites U with the next d's first PV only after the
         // next P arrives, which this warp publishes after these loads

@@ -18,13 +18,15 @@
 // with ONE running max / sum per row across all (d, j2), so O and U are
 // rescaled together (only when the max grows by > 8 in log2 units).
 //
-// MIMW roles (one CTA = 128 query rows of one (batch, head), 8 warps):
+// MIMW roles (one CTA = 128 query rows of one (batch, head), 12 warps):
 //   warp 0     TMA producer of the K2/V2 tile ring (repeated for every d)
 //   warp 1     TMEM allocator + single-thread MMA issuer, running two S tiles
 //              ahead: S(n+2) is issued right after PV(n) (tcgen05.mma ops of
 //              one thread execute in order, so it may overwrite P_n)
-//   warps 2-5  softmax, U -> O fold, epilogue (1 row/thread)
-//   warps 6-7  operand prep (2 rows/thread): Q'_{d+1} = q (.) k1[i-d-1] into
+//   warps 2-9  two softmax warpgroups, each one row/thread over half the
+//              keys of the step (and half the head dim of U / O); row max
+//              exchanged through smem: softmax, U -> O fold, epilogue
+//   warps 10-11 operand prep (2 rows/thread): Q'_{d+1} = q (.) k1[i-d-1] into
 //              the Q' double buffer and the v1[i-d] rows of the fold into smem,
 //              off the softmax warps' critical path (their global-load latency
 //              was ~25% of the kernel, measured)
@@ -49,12 +51,13 @@ constexpr int BKV = 128;
 constexpr int NSLOT = 4;
 constexpr int TILE_BYTES = BKV * D * 2;     // 32 KiB
 constexpr int HALF_BYTES = TILE_BYTES / 2;  // one 64-column swizzle panel
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;
 constexpr int SMEM_QP = 0;                               // 2 Q' buffers
 constexpr int SMEM_KV = 2 * TILE_BYTES;                  // K2/V2 ring
 constexpr int SMEM_V1 = SMEM_KV + NSLOT * TILE_BYTES;     // v1[i - d] rows of the fold
 constexpr int SMEM_BAR = SMEM_V1 + TILE_BYTES;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
+constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024 + 1024;  // barriers, max/sum exchange, align
+static_assert(SMEM_TOTAL <= 232448, "smem");
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);
 constexpr uint32_t TM_S = 0, TM_U = 256, TM_O = 384;  // S buffer b at TM_S + 128 b
@@ -116,8 +119,8 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     }
     mbar_init(s_full(0), 1);
     mbar_init(s_full(1), 1);
-    mbar_init(p_full(0), 4);
-    mbar_init(p_full(1), 4);
+    mbar_init(p_full(0), 8);
+    mbar_init(p_full(1), 8);
     mbar_init(u_done(0), 1);
     mbar_init(u_done(1), 1);
     for (int s = 0; s < NSLOT; ++s) {
@@ -125,7 +128,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       mbar_init(kv_empty(s), 1);
     }
     mbar_init(v1_full, 2);
-    mbar_init(v1_empty, 4);
+    mbar_init(v1_empty, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
@@ -136,21 +139,28 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
 
   if (warp == 0) {
     // ================= TMA producer: K2_t, V2_t for every (d, t) =================
+    // Ring positions follow the MMA warp's consumption order
+    //   K(0) K(1) | V(0) K(2) | V(1) K(3) | ... (S runs two steps ahead of PV),
+    // so a K tile never queues behind a V slot that waits on a PV.
     if (lane == 0) {
       int slot = 0;
       uint32_t ph = 0;
-      for (int n = 0; n < nsteps; ++n) {
+      auto load = [&](bool is_k, int n) {
         const int t = lo + n % ntile;
+        mbar_wait(kv_empty(slot), ph ^ 1, 70);
+        mbar_arrive_expect_tx(kv_full(slot), TILE_BYTES);
+        const uint32_t dst = sbase + SMEM_KV + slot * TILE_BYTES;
+        const CUtensorMap *tm = is_k ? &tmK2 : &tmV2;
+        tma_load_3d(dst, tm, kv_full(slot), 0, t * BKV, bh);
+        tma_load_3d(dst + HALF_BYTES, tm, kv_full(slot), 64, t * BKV, bh);
+        if (++slot == NSLOT) { slot = 0; ph ^= 1; }
+      };
+      if (nsteps > 0) load(true, 0);
+      if (nsteps > 1) load(true, 1);
 #pragma unroll 1
-        for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(kv_empty(slot), ph ^ 1, 70);
-          mbar_arrive_expect_tx(kv_full(slot), TILE_BYTES);
-          const uint32_t dst = sbase + SMEM_KV + slot * TILE_BYTES;
-          const CUtensorMap *tm = kv == 0 ? &tmK2 : &tmV2;
-          tma_load_3d(dst, tm, kv_full(slot), 0, t * BKV, bh);
-          tma_load_3d(dst + HALF_BYTES, tm, kv_full(slot), 64, t * BKV, bh);
-          if (++slot == NSLOT) { slot = 0; ph ^= 1; }
-        }
+      for (int n = 0; n < nsteps; ++n) {
+        load(false, n);
+        if (n + 2 < nsteps) load(true, n + 2);
       }
     }
   } else if (warp == 1) {
@@ -158,15 +168,20 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     constexpr uint32_t HI_KMAJ = (1024u >> 4) | (1u << 14) | (2u << 29);
     constexpr uint32_t LO_KMAJ = (16u >> 4) << 16;
     constexpr uint32_t LO_VMN = ((uint32_t)HALF_BYTES >> 4) << 16;
-    auto ring_wait = [&](int pos) { mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71); };
+    int rpos = 0;  // ring position: the MMA consumes in the producer's order
+    auto ring_next = [&]() {
+      const int pos = rpos++;
+      mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71);
+      return pos % NSLOT;
+    };
     auto issue_S = [&](int n) {  // S of step n = (d, t) into buffer n & 1
       const int d = n / ntile;
       const int t = n % ntile;
       if (t == 0) mbar_wait(qp_full(d & 1), (d >> 1) & 1, 72);
-      ring_wait(2 * n);
+      const int kslot = ring_next();
       tc_fence_after();
       const uint32_t qa = (sbase + SMEM_QP + (d & 1) * TILE_BYTES) >> 4;
-      const uint32_t kb = (sbase + SMEM_KV + ((2 * n) % NSLOT) * TILE_BYTES) >> 4;
+      const uint32_t kb = (sbase + SMEM_KV + kslot * TILE_BYTES) >> 4;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -175,25 +190,25 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
                         make_desc(LO_KMAJ | (kb + off), HI_KMAJ), IDESC_S, k != 0);
         }
         mma_commit(s_full(n & 1));
-        mma_commit(kv_empty((2 * n) % NSLOT));
+        mma_commit(kv_empty(kslot));
         if (t == ntile - 1) mma_commit(qp_empty(d & 1));  // last read of Q'_d
       }
       __syncwarp();
     };
     auto issue_PV = [&](int n) {
       const int t = n % ntile;
-      ring_wait(2 * n + 1);
+      const int vslot = ring_next();
       mbar_wait(p_full(n & 1), (uint32_t)((n >> 1) & 1), 74);
       tc_fence_after();
-      const uint32_t vb = (sbase + SMEM_KV + ((2 * n + 1) % NSLOT) * TILE_BYTES) >> 4;
+      const uint32_t vb = (sbase + SMEM_KV + vslot * TILE_BYTES) >> 4;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          mma_f16_ts<1>(tmem + TM_U, tmem + TM_S + 128 * (n & 1) + k * 8,
+          mma_f16_ts<1>(tmem + TM_U, tmem + TM_S + 128 * (n & 1) + 64 * (k >> 2) + 8 * (k & 3),
                         make_desc(LO_VMN | (vb + k * (2048 >> 4)), HI_KMAJ), IDESC_PV,
                         (t != 0 || k != 0) ? 1u : 0u);
         mma_commit(u_done(n & 1));
-        mma_commit(kv_empty((2 * n + 1) % NSLOT));
+        mma_commit(kv_empty(vslot));
       }
       __syncwarp();
     };
@@ -203,9 +218,9 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       issue_PV(n);
       if (n + 2 < nsteps) issue_S(n + 2);  // overwrites P_n: after PV(n) in issue order
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 10) {
     // ================= operand prep: Q'_d and v1 rows (rows r, r + 32) =================
-    const int pw0 = (warp - 6) * 64 + (int)lane;
+    const int pw0 = (warp - 10) * 64 + (int)lane;
     // ---- Q'_d = q (.) k1[i - d] into smem buffer d&1 (SW128 K-major) ----
     auto prep_qp = [&](int d) {
       if (d >= 2) mbar_wait(qp_empty(d & 1), ((d >> 1) & 1) ^ 1, 75);
@@ -219,19 +234,23 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       const int j1 = i - d;
       const bool ok = row_live && j1 >= 0;
       const uint4 *kv = reinterpret_cast<const uint4 *>(p.k1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
-#pragma unroll 4
-      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 bf16
-        uint4 w = make_uint4(0, 0, 0, 0);
-        if (ok) {
-          const uint4 a = __ldg(qv + c), b = __ldg(kv + c);
-          const uint32_t *pa = &a.x, *pb = &b.x;
-          uint32_t *pw = &w.x;
+      // all 32 loads of the row in flight at once (one L2 round trip per row)
+      uint4 a[16], bk[16];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pa + e));
-            const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pb + e));
-            pw[e] = pack_bf16(fa.x * fb.x, fa.y * fb.y);
-          }
+      for (int c = 0; c < 16; ++c) {
+        a[c] = ok ? __ldg(qv + c) : make_uint4(0, 0, 0, 0);
+        bk[c] = ok ? __ldg(kv + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 bf16
+        uint4 w;
+        const uint32_t *pa = &a[c].x, *pb = &bk[c].x;
+        uint32_t *pw = &w.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pa + e));
+          const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pb + e));
+          pw[e] = pack_bf16(fa.x * fb.x, fa.y * fb.y);
         }
         const int panel = c >> 3, cc = c & 7;
         st_shared_v4(buf + panel * HALF_BYTES + (row >> 3) * 1024 + (row & 7) * 128 +
@@ -246,19 +265,23 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     // ---- v1[i - d] row for the fold of d: 16-B chunk c of row r at c ^ (r & 15) ----
     auto prep_v1 = [&](int d) {
       if (d >= 1) mbar_wait(v1_empty, (uint32_t)((d - 1) & 1), 78);
-#pragma unroll 1
+      uint4 w[2][16];  // both rows' loads in flight at once
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int row = pw0 + 32 * h;
-        const int i = i0 + row;
+        const int i = i0 + pw0 + 32 * h;
         const int j1 = i - d;
         const bool ok = i < p.seq && j1 >= 0;
         const uint4 *vv = reinterpret_cast<const uint4 *>(p.v1 + ((size_t)bh * p.seq + max(j1, 0)) * D);
-        uint4 w[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) w[c] = ok ? __ldg(vv + c) : make_uint4(0, 0, 0, 0);
+        for (int c = 0; c < 16; ++c) w[h][c] = ok ? __ldg(vv + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = pw0 + 32 * h;
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          st_shared_v4(sbase + SMEM_V1 + row * 256 + ((c ^ (row & 15)) << 4), w[c].x, w[c].y, w[c].z, w[c].w);
+          st_shared_v4(sbase + SMEM_V1 + row * 256 + ((c ^ (row & 15)) << 4), w[h][c].x, w[h][c].y,
+                       w[h][c].z, w[h][c].w);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(v1_full);
@@ -270,15 +293,29 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     }
   } else if (warp >= 2) {
     // ================= softmax / U->O fold / epilogue =================
+    // Two warpgroups split each step's 128 keys (g = 0: keys 0-63, g = 1:
+    // 64-127) and the head dim of U / O the same way; the row max is
+    // exchanged through smem every step (one named barrier per lane quarter),
+    // so both keep the same running max and rescale decisions.
     const int q = warp & 3;
+    const int g = (warp - 2) >> 2;
     const int row = q * 32 + (int)lane;  // row of the tile == TMEM lane
     const int i = i0 + row;
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
     const bool row_live = i < p.seq;
+    const uint32_t xbuf = sbase + SMEM_BAR + 256;  // [2 groups][128 rows] f32
     float m_used = -INFINITY, l = 0.f;
     auto wait_pv = [&](int k) {  // PV of step k complete
       mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77);
       tc_fence_after();
+    };
+    auto exchange = [&](float v) {  // the other group's value for this row
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xbuf + (g * 128 + row) * 4), "f"(v) : "memory");
+      named_bar_sync(1 + q, 64);
+      float o;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(xbuf + ((g ^ 1) * 128 + row) * 4) : "memory");
+      named_bar_sync(5 + q, 64);  // both read before either writes the next value
+      return o;
     };
     bool o_live = false;  // O holds a folded U
     const float sl = p.scale_pos ? p.scale_log2 : 1.f;
@@ -288,27 +325,25 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       const int t = n % ntile;
       const int j1 = i - d;
       const int b = n & 1;
-      // ---- S of step n ----
+      // ---- S of step n (this group's 64 keys) ----
       mbar_wait(s_full(b), (uint32_t)((n >> 1) & 1), 76);
       tc_fence_after();
-      uint32_t s[128];
-      const uint32_t t_s = tmem + t_lane + TM_S + 128 * b;
+      uint32_t s[64];
+      const uint32_t t_s = tmem + t_lane + TM_S + 128 * b + 64 * g;
       tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
       tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      tmem_ld_32x32b_x32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-      tmem_ld_32x32b_x32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
       tmem_ld_wait();
       // mask: j2 in [i - w2 + 1, i] and < seq, valid query row, valid K1 row.
       // Uniform fast path: the tile is inside every row's window.
-      const int k0 = (lo + t) * BKV;
-      const bool need_mask = (k0 + BKV - 1 > i0) || (k0 < i0 + BQ - p.w2) || (k0 + BKV > p.seq) ||
-                             (i0 + BQ > p.seq) || (i0 < d) || !p.scale_pos;
+      const int k0 = (lo + t) * BKV + 64 * g;
+      const bool need_mask = ((lo + t) * BKV + BKV - 1 > i0) || ((lo + t) * BKV < i0 + BQ - p.w2) ||
+                             ((lo + t) * BKV + BKV > p.seq) || (i0 + BQ > p.seq) || (i0 < d) || !p.scale_pos;
       const bool live = row_live && j1 >= 0;
       if (need_mask) {
         const int c_lo = i - p.w2 + 1 - k0;
         const int c_hi = min(i, p.seq - 1) - k0;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
+        for (int c = 0; c < 64; ++c) {
           float v = __uint_as_float(s[c]);
           if (!p.scale_pos) v *= p.scale_log2;
           if (!live || c < c_lo || c > c_hi) v = -INFINITY;
@@ -317,12 +352,13 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       }
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 128; c += 8) {
+      for (int c = 0; c < 64; c += 8) {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
       }
-      const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
+      float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
+      mx = fmaxf(mx, exchange(mx));
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
@@ -334,9 +370,9 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
       const uint64_t nm2 = f2_pack(nm, nm);
       uint64_t acc2[4] = {0, 0, 0, 0};
-      uint32_t pk[64];
+      uint32_t pk[32];
 #pragma unroll
-      for (int e = 0; e < 64; ++e) {
+      for (int e = 0; e < 32; ++e) {
         const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), sl2, nm2);
         const uint64_t p2 = ex2_mufu2(x2);
         acc2[e & 3] = f2_add(acc2[e & 3], p2);
@@ -354,7 +390,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
         // U (this d's partial sum, if any PV of it ran) and O carry the old max
         if (n >= 1) wait_pv(n - 1);
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 64 * g; c < 64 * g + 64; c += 32) {
           uint32_t o[32];
           if (t > 0) {
             tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, o);
@@ -374,9 +410,8 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
           }
         }
       }
-#pragma unroll
-      for (int c = 0; c < 64; c += 16)
-        tmem_st_32x32b_x16(t_s + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
+      tmem_st_32x32b_x16(t_s, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+      tmem_st_32x32b_x16(t_s + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -386,15 +421,15 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
         wait_pv(n);
         mbar_wait(v1_full, (uint32_t)(d & 1), 79);
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 64 * g; c < 64 * g + 64; c += 32) {
           uint32_t u[32], o[32];
           tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, u);
           if (o_live) tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
+          for (int gg = 0; gg < 4; ++gg) {
             uint4 w;
-            const int ch = c / 8 + g;
+            const int ch = c / 8 + gg;
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
                          : "r"(sbase + SMEM_V1 + row * 256 + ((ch ^ (row & 15)) << 4)));
@@ -402,7 +437,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pw + e));
-              const int x = g * 8 + e * 2;
+              const int x = gg * 8 + e * 2;
               const float b0 = o_live ? __uint_as_float(o[x]) : 0.f;
               const float b1 = o_live ? __uint_as_float(o[x + 1]) : 0.f;
               o[x] = __float_as_uint(b0 + f.x * __uint_as_float(u[x]));
@@ -422,12 +457,13 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       }
     }
     // ---------------- epilogue: O / l, lse ----------------
+    l += exchange(l);  // both groups' partial sums
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
-    if (row_live && p.lse != nullptr)
+    if (g == 0 && row_live && p.lse != nullptr)
       p.lse[(size_t)bh * p.seq + i] = (m_used + __log2f(l)) * (1.0f / LOG2E);
     uint4 *orow = reinterpret_cast<uint4 *>(p.o + ((size_t)bh * p.seq + min(i, p.seq - 1)) * D);
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 32) {
+    for (int c = 64 * g; c < 64 * g + 64; c += 32) {
       uint32_t o[32];
       tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
       tmem_ld_wait();

@@ -616,7 +616,8 @@ def bench_simplicial(args, rank, ws, local):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
                          "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
                          "peak_source": f"{pk['src']} bf16 burst",
-                         "algorithmic_flop_per_launch": flop_head * (r1 - r0), "traffic": None},
+                         "algorithmic_flop_per_launch": flop_head * (r1 - r0),
+                         "traffic": traffic("simplicial")},
             "clocks": clocks}
 
 
@@ -757,7 +758,7 @@ def bench_multidevice(args, rank, ws, local):
                         "frac_of_target": round(target / per, 4),
                         "remote_bytes_per_rank": remote_bytes,
                         "target_rule": "max(FLOP / bf16 peak, remote bytes / 770 GB/s NVLink)",
-                        "traffic": None},
+                        "traffic": traffic("multi_device_gemm")},
            "clocks": clocks}
     if serial is not None:
         out["gather_then_gemm_ms"] = round(serial * 1e3, 4)

@@ -20,7 +20,7 @@
 //   dK  += dS^T Q_i       (TS)
 //   dQ_i^T = K^T dS^T     (SS: K MN-major, dS^T staged in smem)
 // MIMW roles (16 warps):
-//   warp 0      TMA producer: K, V once; Q_i, dO_i, lse_i, D_i per step (2 stages)
+//   warp 0      TMA producer: K, V once; Q_i, dO_i per step (3 stages)
 //   warp 1      MMA issuer (one elected lane), tcgen05.commit -> mbarriers
 //   warps 4-11  two "softmax" warpgroups, one per 32-query half of the step:
 //               P^T, dS^T from S^T / dP^T (lane = key), P^T / dS^T -> TMEM,
@@ -54,8 +54,8 @@ constexpr int SM_Q = SM_V + 2 * KPANEL;
 constexpr int SM_DO = SM_Q + NST * QT_BYTES;
 constexpr int SM_DS = SM_DO + NST * QT_BYTES;     // 2 x [128 keys][64 queries] bf16, SW128 (16 KiB each)
 constexpr int SM_DQ = SM_DS + 2 * BKV * 128;      // 4 warps x 2 boxes x [32 d][32 q] f32 (32 KiB)
-constexpr int SM_LD = SM_DQ + 4 * 8192;           // NST stages x (lse2[64] + D[64]) f32
-constexpr int SM_BAR = SM_LD + NST * 512;
+constexpr int SM_LD = SM_DQ + 4 * 8192;           // 2 x (lse2[64] + D[64]) f32, softmax warps' double buffer
+constexpr int SM_BAR = SM_LD + 2 * 512;
 static_assert(SM_BAR + 256 + 1024 <= 232448, "smem");
 constexpr int SMEM_TOTAL = SM_BAR + 256 + 1024;
 constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 192, TM_DV = 256, TM_DK = 384;
@@ -173,18 +173,15 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         tma_load_3d(sbase + SM_K + h * KPANEL, &tmK, kv_full, 64 * h, j * BKV, bh);
         tma_load_3d(sbase + SM_V + h * KPANEL, &tmV, kv_full, 64 * h, j * BKV, bh);
       }
-      const size_t row0 = (size_t)bh * p.nq * BQ;
       for (int t = 0; t < n; ++t) {
         const int s = t % NST;
         const int i = q_tile(t);
         mbar_wait(ld_empty(s), ((t / NST) & 1) ^ 1, 1);
-        mbar_arrive_expect_tx(ld_full(s), 2 * QT_BYTES + 512);
+        mbar_arrive_expect_tx(ld_full(s), 2 * QT_BYTES);
         for (int h = 0; h < 2; ++h) {
           tma_load_3d(sbase + SM_Q + s * QT_BYTES + h * QPANEL, &tmQ, ld_full(s), 64 * h, i * BQ, bh);
           tma_load_3d(sbase + SM_DO + s * QT_BYTES + h * QPANEL, &tmDO, ld_full(s), 64 * h, i * BQ, bh);
         }
-        bulk_load(sbase + SM_LD + s * 512, p.lse2 + row0 + (size_t)i * BQ, 256, ld_full(s));
-        bulk_load(sbase + SM_LD + s * 512 + 256, p.dvec + row0 + (size_t)i * BQ, 256, ld_full(s));
       }
     }
   } else if (warp == 1) {
@@ -270,9 +267,24 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     const int krow = qq * 32 + (int)lane;      // key row inside the tile
     const int key = j * BKV + krow;
     const uint32_t t_lane = (uint32_t)(qq * 32) << 16;
+    const int ctid = (int)threadIdx.x - 128;  // 0..255 over the softmax warps
+    if (n > 0 && ctid < 128) {
+      const float *src = ctid < 64 ? p.lse2 : p.dvec;
+      *reinterpret_cast<float *>(smem + SM_LD + ctid * 4) =
+          __ldg(src + ((size_t)bh * p.nq + q_tile(0)) * BQ + (ctid & 63));
+    }
+    named_bar_sync(1, 256);
     for (int t = 0; t < n; ++t) {
       const int s = t & 1;
       const int i = q_tile(t);
+      // lse2 / D of the NEXT step: one value per thread (threads 0-63 lse2,
+      // 64-127 D), loaded now, published into the smem double buffer at the end
+      // of this step (named barrier among the softmax warps)
+      float pre = 0.f;
+      if (t + 1 < n && ctid < 128) {
+        const float *src = ctid < 64 ? p.lse2 : p.dvec;
+        pre = __ldg(src + ((size_t)bh * p.nq + q_tile(t + 1)) * BQ + (ctid & 63));
+      }
       mbar_wait(s_full, t & 1, 7);
       tc_fence_after();
       uint32_t sv[32], dp[32];
@@ -283,16 +295,12 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dp_free);
-      // lse2 / D of this half's 32 queries (the stage's ld_full also covers them)
-      mbar_wait(ld_full(t % NST), (t / NST) & 1, 8);
-      const float *lse2 = reinterpret_cast<const float *>(smem + SM_LD + (t % NST) * 512) + 32 * ch;
-      const float *dv = lse2 + 64;
       const int q0 = i * BQ + 32 * ch;
       uint32_t pk[16], dk2[16];
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 l4 = *reinterpret_cast<const float4 *>(lse2 + 4 * c4);
-        const float4 d4 = *reinterpret_cast<const float4 *>(dv + 4 * c4);
+        const float4 l4 = *reinterpret_cast<const float4 *>(smem + SM_LD + (t & 1) * 512 + (32 * ch + 4 * c4) * 4);
+        const float4 d4 = *reinterpret_cast<const float4 *>(smem + SM_LD + (t & 1) * 512 + 256 + (32 * ch + 4 * c4) * 4);
         const float la[4] = {l4.x, l4.y, l4.z, l4.w};
         const float da[4] = {d4.x, d4.y, d4.z, d4.w};
         float pv[4], dsv[4];
@@ -327,6 +335,8 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (ctid < 128) *reinterpret_cast<float *>(smem + SM_LD + ((t + 1) & 1) * 512 + ctid * 4) = pre;
+      named_bar_sync(1, 256);  // next step's lse2 / D visible; this step's reads done
     }
     // ---------------- epilogue: dV, dK (x scale) -> bf16 HBM ----------------
     if (n > 0) {

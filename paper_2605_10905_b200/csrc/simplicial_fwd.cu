@@ -95,8 +95,10 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
   auto u_done = [&](int b) { return bars + 64 + 8 * b; };
   auto kv_full = [&](int s) { return bars + 80 + 8 * s; };
   auto kv_empty = [&](int s) { return bars + 80 + 8 * NSLOT + 8 * s; };
-  const uint32_t v1_full = bars + 80 + 16 * NSLOT, v1_empty = v1_full + 8;
-  const uint32_t tmem_slot = v1_full + 16;
+  // v1 row buffer handoff prep warps <-> softmax warps: named barriers 9 (full)
+  // and 10 (empty) over the 2 + 8 warps (producer/consumer bar.arrive / bar.sync)
+  constexpr uint32_t V1_FULL = 9, V1_EMPTY = 10, V1_THREADS = 320;
+  const uint32_t tmem_slot = bars + 80 + 16 * NSLOT + 16;
   volatile uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + SMEM_BAR + 96 + 16 * NSLOT);
 
   const int warp = threadIdx.x / 32;
@@ -127,8 +129,6 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
     }
-    mbar_init(v1_full, 2);
-    mbar_init(v1_empty, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
@@ -264,7 +264,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     };
     // ---- v1[i - d] row for the fold of d: 16-B chunk c of row r at c ^ (r & 15) ----
     auto prep_v1 = [&](int d) {
-      if (d >= 1) mbar_wait(v1_empty, (uint32_t)((d - 1) & 1), 78);
+      if (d >= 1) named_bar_sync(V1_EMPTY, V1_THREADS);  // the fold of d - 1 has read the rows
       uint4 w[2][16];  // both rows' loads in flight at once
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -284,7 +284,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
                        w[h][c].z, w[h][c].w);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(v1_full);
+      named_bar_arrive(V1_FULL, V1_THREADS);
     };
     if (nd > 0) prep_qp(0);
     for (int d = 0; d < nd; ++d) {
@@ -419,7 +419,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       if (t == ntile - 1) {
         // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
         wait_pv(n);
-        mbar_wait(v1_full, (uint32_t)(d & 1), 79);
+        named_bar_sync(V1_FULL, V1_THREADS);
 #pragma unroll 1
         for (int c = 64 * g; c < 64 * g + 64; c += 32) {
           uint32_t u[32], o[32];
@@ -449,7 +449,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
         }
         tmem_st_wait();
         __syncwarp();
-        if (lane == 0) mbar_arrive(v1_empty);  // v1 rows of d read
+        if (d + 1 < nd) named_bar_arrive(V1_EMPTY, V1_THREADS);  // v1 rows of d read
         o_live = true;
         // the PV issuer overwrites U with the next d's first PV only after the
         // next P arrives, which this warp publishes after these loads

@@ -78,6 +78,21 @@ __device__ __forceinline__ void kv2_range(int i0, const Params &p, int &lo, int 
   hi = min(i0 + BQ - 1, p.seq - 1) / BKV;
 }
 
+#ifdef MIMW_SIMP_TRACE
+// per-warp cycle accounting of the first 4 CTAs (tools/simp_trace.py):
+// [cta][warp][8] = role-specific wait buckets, [7] = total
+__device__ unsigned long long g_simp_trace[4 * 12 * 8];
+#define TR_DECL unsigned long long tr_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; const long long tr_t0 = clock64();
+#define TR(i, stmt) do { const long long t_ = clock64(); stmt; tr_[i] += clock64() - t_; } while (0)
+#define TR_END \
+  if (blockIdx.x < 4 && lane == 0) { tr_[7] = clock64() - tr_t0; \
+    for (int e_ = 0; e_ < 8; ++e_) g_simp_trace[(blockIdx.x * 12 + warp) * 8 + e_] = tr_[e_]; }
+#else
+#define TR_DECL
+#define TR(i, stmt) stmt
+#define TR_END
+#endif
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
                       Params p) {
@@ -136,6 +151,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  TR_DECL
 
   if (warp == 0) {
     // ================= TMA producer: K2_t, V2_t for every (d, t) =================
@@ -147,7 +163,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       uint32_t ph = 0;
       auto load = [&](bool is_k, int n) {
         const int t = lo + n % ntile;
-        mbar_wait(kv_empty(slot), ph ^ 1, 70);
+        TR(0, mbar_wait(kv_empty(slot), ph ^ 1, 70));
         mbar_arrive_expect_tx(kv_full(slot), TILE_BYTES);
         const uint32_t dst = sbase + SMEM_KV + slot * TILE_BYTES;
         const CUtensorMap *tm = is_k ? &tmK2 : &tmV2;
@@ -171,13 +187,13 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     int rpos = 0;  // ring position: the MMA consumes in the producer's order
     auto ring_next = [&]() {
       const int pos = rpos++;
-      mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71);
+      TR(1, mbar_wait(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 71));
       return pos % NSLOT;
     };
     auto issue_S = [&](int n) {  // S of step n = (d, t) into buffer n & 1
       const int d = n / ntile;
       const int t = n % ntile;
-      if (t == 0) mbar_wait(qp_full(d & 1), (d >> 1) & 1, 72);
+      if (t == 0) TR(2, mbar_wait(qp_full(d & 1), (d >> 1) & 1, 72));
       const int kslot = ring_next();
       tc_fence_after();
       const uint32_t qa = (sbase + SMEM_QP + (d & 1) * TILE_BYTES) >> 4;
@@ -198,7 +214,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     auto issue_PV = [&](int n) {
       const int t = n % ntile;
       const int vslot = ring_next();
-      mbar_wait(p_full(n & 1), (uint32_t)((n >> 1) & 1), 74);
+      TR(3, mbar_wait(p_full(n & 1), (uint32_t)((n >> 1) & 1), 74));
       tc_fence_after();
       const uint32_t vb = (sbase + SMEM_KV + vslot * TILE_BYTES) >> 4;
       if (elect_one()) {
@@ -223,7 +239,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     const int pw0 = (warp - 10) * 64 + (int)lane;
     // ---- Q'_d = q (.) k1[i - d] into smem buffer d&1 (SW128 K-major) ----
     auto prep_qp = [&](int d) {
-      if (d >= 2) mbar_wait(qp_empty(d & 1), ((d >> 1) & 1) ^ 1, 75);
+      if (d >= 2) TR(1, mbar_wait(qp_empty(d & 1), ((d >> 1) & 1) ^ 1, 75));
       const uint32_t buf = sbase + SMEM_QP + (d & 1) * TILE_BYTES;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
@@ -264,7 +280,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     };
     // ---- v1[i - d] row for the fold of d: 16-B chunk c of row r at c ^ (r & 15) ----
     auto prep_v1 = [&](int d) {
-      if (d >= 1) named_bar_sync(V1_EMPTY, V1_THREADS);  // the fold of d - 1 has read the rows
+      if (d >= 1) TR(2, named_bar_sync(V1_EMPTY, V1_THREADS));  // the fold of d - 1 has read the rows
       uint4 w[2][16];  // both rows' loads in flight at once
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -306,15 +322,15 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     const uint32_t xbuf = sbase + SMEM_BAR + 256;  // [2 groups][128 rows] f32
     float m_used = -INFINITY, l = 0.f;
     auto wait_pv = [&](int k) {  // PV of step k complete
-      mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77);
+      TR(2, mbar_wait(u_done(k & 1), (uint32_t)((k >> 1) & 1), 77));
       tc_fence_after();
     };
     auto exchange = [&](float v) {  // the other group's value for this row
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(xbuf + (g * 128 + row) * 4), "f"(v) : "memory");
-      named_bar_sync(1 + q, 64);
+      TR(3, named_bar_sync(1 + q, 64));
       float o;
       asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(xbuf + ((g ^ 1) * 128 + row) * 4) : "memory");
-      named_bar_sync(5 + q, 64);  // both read before either writes the next value
+      TR(3, named_bar_sync(5 + q, 64));  // both read before either writes the next value
       return o;
     };
     bool o_live = false;  // O holds a folded U
@@ -326,7 +342,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       const int j1 = i - d;
       const int b = n & 1;
       // ---- S of step n (this group's 64 keys) ----
-      mbar_wait(s_full(b), (uint32_t)((n >> 1) & 1), 76);
+      TR(1, mbar_wait(s_full(b), (uint32_t)((n >> 1) & 1), 76));
       tc_fence_after();
       uint32_t s[64];
       const uint32_t t_s = tmem + t_lane + TM_S + 128 * b + 64 * g;
@@ -419,7 +435,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       if (t == ntile - 1) {
         // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
         wait_pv(n);
-        named_bar_sync(V1_FULL, V1_THREADS);
+        TR(4, named_bar_sync(V1_FULL, V1_THREADS));
 #pragma unroll 1
         for (int c = 64 * g; c < 64 * g + 64; c += 32) {
           uint32_t u[32], o[32];
@@ -481,6 +497,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     }
   }
 
+  TR_END
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -518,3 +535,16 @@ cudaError_t simplicial_fwd_launch(const SimplicialArgs &a, cudaStream_t stream) 
 }
 
 }  // namespace mimw
+
+// Debug hook (not in the public header): the per-warp cycle buckets of the
+// first 4 CTAs when built with -DMIMW_SIMP_TRACE (tools/simp_trace.py).
+extern "C" int mimw_b200_debug_simplicial_trace(unsigned long long *host, int n) {
+#ifdef MIMW_SIMP_TRACE
+  if (n > 4 * 12 * 8) n = 4 * 12 * 8;
+  return cudaMemcpyFromSymbol(host, mimw::g_simp_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 3;
+#else
+  (void)host;
+  (void)n;
+  return 2;
+#endif
+}

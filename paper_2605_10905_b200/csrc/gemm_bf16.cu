@@ -32,7 +32,6 @@
 #include "tma_host.h"
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 
 namespace mimw {
@@ -168,7 +167,6 @@ constexpr int COMM_SLAB = 256;   // K columns per readiness counter
 // N columns x R K rows.  R = box rows (32 / 64 / 128: 16 / 32 / 64 KiB).
 constexpr int COMM_W = 256;
 constexpr int COMM_MAX_BUFS = 24;
-constexpr int COMM_SIG = 16;     // ring of pending slab signals per agent (lag < COMM_SIG)
 struct GatherSched : SchedT<1> {
   static constexpr bool kGather = true;
   CUtensorMap ga[MAX_SPLITS], gb[MAX_SPLITS];          // GEMM operands, rotation order (q = 0 local)
@@ -180,8 +178,6 @@ struct GatherSched : SchedT<1> {
   int agents;                 // independent TMA copy pipelines per comm CTA (one thread each)
   int lag;                    // stores in flight before a slab signal waits for completion
   int pull;                   // 0: this rank pulls nothing (no rows), barrier only
-  int sigmode;                // slab signals: 4 = signaler thread (default), 3 = agent release,
-                              // 1 = agent relaxed atomic (experiments: MIMW_MD_SIGMODE)
   uint32_t *ctr;              // [MAX_SPLITS * max_slabs] slab counters + GO + PULLED, zeroed per launch
   uint32_t *pad_local;        // this rank's signal pad: IN[MAX_SPLITS], OUT[MAX_SPLITS]; null = no barrier
   uint32_t *pad_peer[MAX_SPLITS];
@@ -230,9 +226,8 @@ struct BoxCursor {
 // scope; atomics also keep compute-sanitizer's racecheck, which does not model
 // plain acquire/release flags, out of the message passing)
 __device__ __forceinline__ void st_release_cta_shared(uint32_t addr, uint32_t v) {
-  uint32_t prev;
-  asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(addr), "r"(v) : "memory");
-  (void)prev;
+  asm volatile("{\n\t.reg .b32 prev;\n\tatom.release.cta.shared::cta.exch.b32 prev, [%0], %1;\n\t}" ::"r"(addr), "r"(v)
+               : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_cta_shared(uint32_t addr) {
   uint32_t v;
@@ -258,8 +253,6 @@ __device__ __forceinline__ void gather_agent(const GatherSched &sp, uint32_t buf
   cur.init(sp, agent);
   const CUtensorMap *dmap[COMM_MAX_BUFS];
   int dx[COMM_MAX_BUFS], dy[COMM_MAX_BUFS];
-  uint32_t *dctr[COMM_MAX_BUFS];
-  uint32_t *sig[COMM_SIG];
   auto issue_load = [&](int idx) {
     const int slot = idx % nb;
     const int k0 = cur.j * COMM_SLAB;
@@ -274,22 +267,17 @@ __device__ __forceinline__ void gather_agent(const GatherSched &sp, uint32_t buf
     }
     dx[slot] = x;
     dy[slot] = y;
-    dctr[slot] = cur.ctr(sp);
     const uint32_t bar = bar0 + 8 * slot;
     mbar_arrive_expect_tx(bar, box_bytes);
     tma_load_2d(buf0 + slot * box_bytes, src, bar, x, y);
     cur.advance(sp, nagents);
   };
-  auto landed = [&](int count, int first) {  // boxes [first, count) have landed
+  // boxes [0, count) have landed: publish the count to the signaler (measured:
+  // a red.release.gpu issued here waits for this thread's in-flight TMA
+  // traffic and halved the copy rate)
+  auto landed = [&](int count) {
     fence_proxy_async_global();
-    if (sp.sigmode == 4) {
-      st_release_cta_shared(mbox, (uint32_t)count);
-    } else {
-      for (int i = first; i < count; ++i) {
-        if (sp.sigmode & 2) red_release_gpu_add(sig[i % COMM_SIG], 1u);
-        else atomicAdd(sig[i % COMM_SIG], 1u);
-      }
-    }
+    st_release_cta_shared(mbox, (uint32_t)count);
   };
   int nl = 0;
   while (nl < nb && cur.live) issue_load(nl++);
@@ -299,7 +287,6 @@ __device__ __forceinline__ void gather_agent(const GatherSched &sp, uint32_t buf
     mbar_wait(bar0 + 8 * slot, (uint32_t)((ns / nb) & 1), 22);
     tma_store_2d(dmap[slot], buf0 + slot * box_bytes, dx[slot], dy[slot]);
     bulk_commit();
-    sig[ns % COMM_SIG] = dctr[slot];
     if (nb == 1) {
       bulk_wait_read<0>();           // single buffer: reload once this store has read it
       if (cur.live) issue_load(nl++);
@@ -309,11 +296,11 @@ __device__ __forceinline__ void gather_agent(const GatherSched &sp, uint32_t buf
     }
     if (ns >= LAG) {
       bulk_wait<LAG>();              // stores <= ns-LAG have landed
-      landed(ns - LAG + 1, ns - LAG);
+      landed(ns - LAG + 1);
     }
   }
   bulk_wait<0>();
-  landed(ns, ns > LAG ? ns - LAG : 0);
+  landed(ns);
 }
 
 // Signaler thread of a comm CTA: replays each agent's box sequence and, as
@@ -417,7 +404,7 @@ __device__ __forceinline__ void gather_comm_cta(const GatherSched &sp, uint32_t 
     const int nb = nbuf / sp.agents;
     gather_agent_lag(sp, ring + warp * nb * box_bytes, bars + 8 * warp * nb, nb,
                      ci * sp.agents + warp, nagents, mbox0 + 4 * warp);
-  } else if (lane0 && warp == 7 && sp.sigmode == 4) {
+  } else if (lane0 && warp == 7) {
     gather_signaler(sp, ci * sp.agents, sp.agents, nagents, mbox0);
   }
   __syncthreads();
@@ -655,7 +642,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           gather_agent_lag(sched, sbase + C::BAR_OFF - C::COMM_EXTRA, bar_base + C::BAR_BYTES,
                            C::COMM_EXTRA / (sched.box * COMM_W * 2), agent, nagents, mbox);
           gather_exit(sched, agent == 0, (uint32_t)nagents);
-        } else if (sched.sigmode == 4) {
+        } else {
           gather_signaler(sched, agent, 1, nagents, mbox);
         }
       }
@@ -1016,7 +1003,6 @@ cudaError_t multi_device_gemm_launch(const MultiDeviceGemmArgs &g, cudaStream_t 
   gs->ctr = ctr;
   gs->max_slabs = L.max_slabs;
   gs->box = box;
-  gs->sigmode = getenv("MIMW_MD_SIGMODE") ? atoi(getenv("MIMW_MD_SIGMODE")) : 4;
   gs->agents = std::min(6, std::max(1, g.comm_agents > 0 ? g.comm_agents : 2));  // warps 0..5
   gs->lag = g.comm_lag > 0 ? g.comm_lag : (distributed ? 4 : 8);
   gs->rbox = (int)((g.rows + box - 1) / box);

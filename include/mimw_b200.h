@@ -47,6 +47,9 @@ extern "C" {
 #define MIMW_PREC_BF16 0          /* inputs rounded to bf16 (RNE), fp32 accumulate */
 #define MIMW_PREC_F32_BF16X3 1    /* split-bf16 x3 on tensor cores: ~1e-6 rel-err,
                                      meets the reference's own 1e-4 GEMM cases */
+#define MIMW_PREC_F32 2           /* attention Tiles: the oracles' f64 score / softmax
+                                     arithmetic on CUDA cores (reference tolerances
+                                     1e-4 / 1e-3; for reference-scale Tiles) */
 
 int mimw_b200_version(void);
 const char *mimw_b200_last_error(void);
@@ -168,6 +171,13 @@ int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, f
  * paper's AFN / ABC rows, PAPER.md:702-716 — no reference oracle) */
 #define MIMW_WINDOW_NONCAUSAL 0
 
+/* Same with a precision: MIMW_PREC_BF16 (the tcgen05 kernel on bf16 inputs,
+ * rel-err ~3e-3, the north-star 1e-2 bar) or MIMW_PREC_F32 (the reference's own
+ * 1e-4, acceptance.cpp:333-355). */
+int mimw_b200_oracle_attention_ex(const float *q, const float *k, const float *v, float *o,
+                                  float *lse, int64_t seq, int64_t d, int64_t w, double scale,
+                                  int32_t precision);
+
 /* Device form: q, k, v, o bf16 [batch, heads, seq, head_dim] contiguous,
  * head_dim == 128; lse fp32 [batch, heads, seq] or NULL.  window >= 1 as in
  * the reference, or MIMW_WINDOW_NONCAUSAL.  Warp-specialized
@@ -202,6 +212,13 @@ int mimw_b200_oracle_simplicial_attention(const float *q, const float *k1, const
                                            const float *k2, const float *v2, float *o, float *lse,
                                            int64_t seq, int64_t d, int64_t w1, int64_t w2,
                                            double scale);
+
+/* Same with a precision (MIMW_PREC_BF16 or MIMW_PREC_F32, which holds the
+ * reference case's 1e-3, simplicial_attention.case). */
+int mimw_b200_oracle_simplicial_attention_ex(const float *q, const float *k1, const float *v1,
+                                              const float *k2, const float *v2, float *o, float *lse,
+                                              int64_t seq, int64_t d, int64_t w1, int64_t w2,
+                                              double scale, int32_t precision);
 
 /* Device form: bf16 [bh, seq, 128] contiguous (bh = batch*heads), lse fp32
  * [bh, seq] or NULL.  Per K1 offset a windowed flash-attention sweep over K2/V2

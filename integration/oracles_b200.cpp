@@ -1,0 +1,81 @@
+// The reference-side binding of the drop-in boundary:
+// the hot-path functions of proj/core/include/mimw/oracles.hpp, with the
+// reference's exact signatures and Tile type, implemented over the C-ABI of
+// libmimw_b200.so (include/mimw_b200.h).  A maintainer compiles this file in
+// place of the corresponding bodies of proj/core/src/oracles.cpp; callers
+// (run_oracle, tools/mimw.cpp, the tests) are unchanged.
+//
+//   oracle_gemm                  oracles.hpp:15-16  -> mimw_b200_oracle_gemm
+//   oracle_multi_device_gemm     oracles.hpp:24-25  -> mimw_b200_oracle_multi_device_gemm
+//   oracle_attention             oracles.hpp:36-37  -> mimw_b200_oracle_attention_ex
+//   oracle_simplicial_attention  oracles.hpp:31-33  -> mimw_b200_oracle_simplicial_attention_ex
+//   oracle_layernorm             oracles.hpp:20-21  -> mimw_b200_oracle_layernorm
+//
+// Errors: the reference reports none (shapes are trusted, oracles.cpp:15);
+// here a non-zero status throws std::runtime_error with
+// mimw_b200_last_error(), the C++ analogue of the reference's .at() throws.
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "mimw/oracles.hpp"  // the reference's header, unmodified (-I proj/core/include)
+#include "mimw_b200.h"
+
+namespace mimw {
+
+namespace {
+void ok(int status) {
+  if (status != MIMW_OK) throw std::runtime_error(std::string("mimw_b200: ") + mimw_b200_last_error());
+}
+Tile shaped(std::vector<std::int64_t> shape) { return Tile(std::move(shape)); }
+// The reference's f32 GEMM cases demand 1e-4 (gemm_pipeline.case:5): split-bf16 x3.
+constexpr int kGemmPrecision = MIMW_PREC_F32_BF16X3;
+// Attention at the reference's tolerances (1e-4 / 1e-3): the f64-arithmetic
+// CUDA-core path.  MIMW_PREC_BF16 selects the tcgen05 kernels (1e-2 bar).
+constexpr int kAttnPrecision = MIMW_PREC_F32;
+}  // namespace
+
+Tile oracle_gemm(const Tile &a, const Tile &b) {
+  const std::int64_t m = a.shape[0], k = a.shape[1], n = b.shape[1];
+  Tile c = shaped({m, n});
+  ok(mimw_b200_oracle_gemm(a.data.data(), b.data.data(), c.data.data(), m, n, k, kGemmPrecision));
+  return c;
+}
+
+Tile oracle_multi_device_gemm(const Tile &a0, const Tile &a1, const Tile &b0, const Tile &b1) {
+  const std::int64_t m = a0.shape[0], k0 = a0.shape[1], k1 = a1.shape[1], n = b0.shape[1];
+  Tile c = shaped({m, n});
+  ok(mimw_b200_oracle_multi_device_gemm(a0.data.data(), a1.data.data(), b0.data.data(), b1.data.data(),
+                                        c.data.data(), m, k0, k1, n, kGemmPrecision));
+  return c;
+}
+
+void oracle_attention(const Tile &q, const Tile &k, const Tile &v, int w, double scale, Tile *o) {
+  const std::int64_t s = q.shape[0], d = q.shape[1];
+  *o = shaped({s, d});
+  ok(mimw_b200_oracle_attention_ex(q.data.data(), k.data.data(), v.data.data(), o->data.data(), nullptr, s, d,
+                                   w, scale, kAttnPrecision));
+}
+
+void oracle_simplicial_attention(const Tile &q, const Tile &k1, const Tile &v1, const Tile &k2,
+                                 const Tile &v2, int w1, int w2, double scale, Tile *o, Tile *lse) {
+  const std::int64_t s = q.shape[0], d = q.shape[1];
+  *o = shaped({s, d});
+  *lse = shaped({s});
+  ok(mimw_b200_oracle_simplicial_attention_ex(q.data.data(), k1.data.data(), v1.data.data(), k2.data.data(),
+                                              v2.data.data(), o->data.data(), lse->data.data(), s, d, w1, w2,
+                                              scale, kAttnPrecision));
+}
+
+void oracle_layernorm(const Tile &x, const Tile &w, const Tile &b, double eps, Tile *y, Tile *mean,
+                      Tile *rstd) {
+  const std::int64_t rows = x.shape[0], n = x.shape[1];
+  *y = shaped({rows, n});
+  if (mean) *mean = shaped({rows});
+  if (rstd) *rstd = shaped({rows});
+  ok(mimw_b200_oracle_layernorm(x.data.data(), w.data.data(), b.data.data(), eps, y->data.data(),
+                                mean ? mean->data.data() : nullptr, rstd ? rstd->data.data() : nullptr, rows,
+                                n));
+}
+
+}  // namespace mimw

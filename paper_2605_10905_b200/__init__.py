@@ -29,7 +29,7 @@ LIB_PATH = os.path.join(PKG, "libmimw_b200.so")
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
 B_KN, B_NK = 0, 1
-PREC_BF16, PREC_F32_BF16X3 = 0, 1
+PREC_BF16, PREC_F32_BF16X3, PREC_F32 = 0, 1, 2
 
 _i64 = C.c_int64
 _vp = C.c_void_p
@@ -70,6 +70,9 @@ def lib() -> C.CDLL:
 def _optional_sigs():
     return {
         "mimw_b200_oracle_attention": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double],
+        "mimw_b200_oracle_attention_ex": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double,
+                                          C.c_int32],
+        "mimw_b200_oracle_simplicial_attention_ex": [_fp] * 7 + [_i64] * 4 + [C.c_double, C.c_int32],
         "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_bwd": [_vp] * 5 + [_vp] + [_vp] * 3 + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
@@ -131,9 +134,12 @@ def oracle_multi_device_gemm(a0, a1, b0, b1, precision: int = PREC_BF16) -> np.n
     return c
 
 
-def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
+def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False,
+                     precision: int = PREC_BF16):
     """``void oracle_attention(q, k, v, int w, double scale, Tile *o)``
-    (oracles.hpp:35-37): windowed causal softmax attention of one [S, D] head."""
+    (oracles.hpp:35-37): windowed causal softmax attention of one [S, D] head.
+    ``precision=PREC_F32`` holds the reference's own 1e-4 (the oracle's f64
+    arithmetic on CUDA cores); the default is the bf16 tcgen05 kernel (1e-2)."""
     L = lib()
     if not hasattr(L, "mimw_b200_oracle_attention"):
         raise MimwError(ERR_UNSUPPORTED, "attention not built")
@@ -141,21 +147,23 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False):
     s, d = q.shape
     o = np.empty((s, d), np.float32)
     lse = np.empty(s, np.float32)
-    _check(L.mimw_b200_oracle_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s, d, w,
-                                        scale))
+    _check(L.mimw_b200_oracle_attention_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s, d, w,
+                                           scale, precision))
     return (o, lse) if with_lse else o
 
 
-def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float):
+def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float,
+                                precision: int = PREC_BF16):
     """``oracle_simplicial_attention`` (oracles.hpp:31-33, oracles.cpp:82-117)
-    on the B200 kernel for one [S, D] head; returns (o, lse)."""
+    on the B200 for one [S, D] head; returns (o, lse).  ``precision`` as for
+    ``oracle_attention`` (PREC_F32 holds the reference case's 1e-3)."""
     q, k1, v1, k2, v2 = map(_f32, (q, k1, v1, k2, v2))
     s, d = q.shape
     o = np.empty((s, d), np.float32)
     lse = np.empty(s, np.float32)
-    _check(lib().mimw_b200_oracle_simplicial_attention(_ptr(q), _ptr(k1), _ptr(v1), _ptr(k2),
-                                                       _ptr(v2), _ptr(o), _ptr(lse), s, d, w1, w2,
-                                                       scale))
+    _check(lib().mimw_b200_oracle_simplicial_attention_ex(_ptr(q), _ptr(k1), _ptr(v1), _ptr(k2),
+                                                          _ptr(v2), _ptr(o), _ptr(lse), s, d, w1,
+                                                          w2, scale, precision))
     return o, lse
 
 
@@ -174,24 +182,29 @@ def oracle_layernorm(x, w, b, eps: float):
 
 def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: int = PREC_BF16):
     """``run_oracle`` (oracles.cpp:147-201) dispatching to the B200 path for
-    the hot-path oracles.  Unknown / off-path names return ``None``."""
+    the hot-path oracles.  Unknown / off-path names return ``None``.
+    ``precision``: PREC_BF16 (the tensor-core kernels, 1e-2) or any reference
+    precision (PREC_F32_BF16X3 / PREC_F32: split-bf16 GEMMs and the f64-arithmetic
+    attention path, which hold the reference cases' own tolerances)."""
     scalars = scalars or {}
+    gp = PREC_F32_BF16X3 if precision else PREC_BF16
     if name == "gemm":
-        return {"c": oracle_gemm(inputs["a"], inputs["b"], precision)}
+        return {"c": oracle_gemm(inputs["a"], inputs["b"], gp)}
     if name == "multi_device_gemm":
         return {"c": oracle_multi_device_gemm(inputs["a0"], inputs["a1"], inputs["b0"],
-                                              inputs["b1"], precision)}
+                                              inputs["b1"], gp)}
     if name == "simplicial_attention":
         o, lse = oracle_simplicial_attention(inputs["q"], inputs["k1"], inputs["v1"], inputs["k2"],
                                              inputs["v2"], int(scalars["w1"]), int(scalars["w2"]),
-                                             scalars["scale"])
+                                             scalars["scale"], PREC_F32 if precision else PREC_BF16)
         return {"o": o, "lse": lse}
     if name == "layernorm":
         return {"y": oracle_layernorm(inputs["x"], inputs["w"], inputs["b"],
                                       scalars.get("eps", 1e-5))[0]}
     if name == "attention":
         return {"o": oracle_attention(inputs["q"], inputs["k"], inputs["v"],
-                                      int(scalars.get("w", 1 << 30)), scalars.get("scale", 1.0))}
+                                      int(scalars.get("w", 1 << 30)), scalars.get("scale", 1.0),
+                                      precision=PREC_F32 if precision else PREC_BF16)}
     return None
 
 

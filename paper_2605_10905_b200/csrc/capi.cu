@@ -18,6 +18,7 @@
 #include "convert.h"
 #include "attention_fwd.h"
 #include "attention_bwd.h"
+#include "attention_f32.h"
 #include "gemm_bf16.h"
 #include "gemm_mxfp8.h"
 #include "layernorm_cluster.h"
@@ -241,11 +242,47 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
 }
 
 
+
+// MIMW_PREC_F32 for the host attention Tiles: the oracles' f64 score /
+// softmax arithmetic on CUDA cores (attention_f32.cu), for callers that hold
+// the reference's own tolerances.
+void host_attention_f32(const float *const *inputs, int n_inputs, float *o, float *lse, int64_t seq,
+                        int64_t d, int64_t w1, int64_t w2, bool simplicial, double scale) {
+  cudaStream_t s = cudaStreamPerThread;
+  const int64_t n = seq * d;
+  DevBuf din(sizeof(float) * (n_inputs * n + seq + n), s);
+  float *f = din.as<float>();
+  for (int t = 0; t < n_inputs; ++t)
+    check_cuda(cudaMemcpyAsync(f + t * n, inputs[t], sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D");
+  float *dout = f + n_inputs * n, *dlse = dout + n;
+  mimw::AttnF32Args a{};
+  a.q = f;
+  a.k1 = f + n;
+  a.v1 = f + 2 * n;
+  a.k2 = simplicial ? f + 3 * n : nullptr;
+  a.v2 = simplicial ? f + 4 * n : nullptr;
+  a.o = dout;
+  a.lse = dlse;
+  a.seq = seq;
+  a.d = d;
+  a.w1 = w1;
+  a.w2 = w2;
+  a.causal = true;
+  a.simplicial = simplicial;
+  a.scale = scale;
+  check_cuda(mimw::attention_f32_launch(a, s), "attention f32 launch");
+  check_cuda(cudaMemcpyAsync(o, dout, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H o");
+  if (lse) check_cuda(cudaMemcpyAsync(lse, dlse, sizeof(float) * seq, cudaMemcpyDeviceToHost, s), "D2H lse");
+  check_cuda(cudaStreamSynchronize(s), "attention f32 execution");
+}
+
 // o[s,d] (+ lse[s]) = oracle_attention(q, k, v, w, scale) for one head of
 // host f32 Tiles (oracles.cpp:119-145).  Head dim is zero-padded to 128 (exact:
 // padded q/k columns add 0 to every score, padded v columns give 0 outputs).
 void host_attention(const float *q, const float *k, const float *v, float *o, float *lse,
-                    int64_t seq, int64_t d, int64_t w, double scale) {
+                    int64_t seq, int64_t d, int64_t w, double scale, int precision = MIMW_PREC_BF16) {
+  require(precision == MIMW_PREC_BF16 || precision == MIMW_PREC_F32, MIMW_ERR_ARG,
+          "precision must be MIMW_PREC_BF16 or MIMW_PREC_F32");
   require(seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
   require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
   require(w >= 1 || seq == 0, MIMW_ERR_ARG, "window must be >= 1");
@@ -257,6 +294,11 @@ void host_attention(const float *q, const float *k, const float *v, float *o, fl
   }
   require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
   require_sm100();
+  if (precision == MIMW_PREC_F32) {
+    const float *in[3] = {q, k, v};
+    host_attention_f32(in, 3, o, lse, seq, d, w, 1, false, scale);
+    return;
+  }
   cudaStream_t s = cudaStreamPerThread;
   const int64_t n = seq * d;
   DevBuf din(sizeof(float) * 3 * n, s);
@@ -337,13 +379,20 @@ void layernorm_checks(const void *x, const void *w, const void *b, const void *y
 // host f32 Tiles; d <= 128 zero-padded to 128 (exact, as host_attention).
 void host_simplicial(const float *q, const float *k1, const float *v1, const float *k2,
                      const float *v2, float *o, float *lse, int64_t seq, int64_t d, int64_t w1,
-                     int64_t w2, double scale) {
+                     int64_t w2, double scale, int precision = MIMW_PREC_BF16) {
+  require(precision == MIMW_PREC_BF16 || precision == MIMW_PREC_F32, MIMW_ERR_ARG,
+          "precision must be MIMW_PREC_BF16 or MIMW_PREC_F32");
   require(seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
   require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
   require((w1 >= 1 && w2 >= 1) || seq == 0, MIMW_ERR_ARG, "windows must be >= 1");
   if (seq == 0) return;
   require(q && k1 && v1 && k2 && v2 && o, MIMW_ERR_ARG, "null pointer");
   require_sm100();
+  if (precision == MIMW_PREC_F32) {
+    const float *in[5] = {q, k1, v1, k2, v2};
+    host_attention_f32(in, 5, o, lse, seq, d, w1, w2, true, scale);
+    return;
+  }
   cudaStream_t s = cudaStreamPerThread;
   const int64_t n = seq * d;
   DevBuf din(sizeof(float) * 5 * n, s);
@@ -432,6 +481,11 @@ int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_
 int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, float *o, float *lse,
                                int64_t seq, int64_t d, int64_t w, double scale) {
   return guarded([&] { host_attention(q, k, v, o, lse, seq, d, w, scale); });
+}
+
+int mimw_b200_oracle_attention_ex(const float *q, const float *k, const float *v, float *o, float *lse,
+                                  int64_t seq, int64_t d, int64_t w, double scale, int32_t precision) {
+  return guarded([&] { host_attention(q, k, v, o, lse, seq, d, w, scale, precision); });
 }
 
 int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o, float *lse,
@@ -566,6 +620,13 @@ int mimw_b200_oracle_simplicial_attention(const float *q, const float *k1, const
                                            int64_t seq, int64_t d, int64_t w1, int64_t w2,
                                            double scale) {
   return guarded([&] { host_simplicial(q, k1, v1, k2, v2, o, lse, seq, d, w1, w2, scale); });
+}
+
+int mimw_b200_oracle_simplicial_attention_ex(const float *q, const float *k1, const float *v1,
+                                              const float *k2, const float *v2, float *o, float *lse,
+                                              int64_t seq, int64_t d, int64_t w1, int64_t w2,
+                                              double scale, int32_t precision) {
+  return guarded([&] { host_simplicial(q, k1, v1, k2, v2, o, lse, seq, d, w1, w2, scale, precision); });
 }
 
 int mimw_b200_simplicial_attention_fwd(const void *q, const void *k1, const void *v1, const void *k2,

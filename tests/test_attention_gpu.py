@@ -98,3 +98,21 @@ def test_device_attention_full_config_sampled(P):
             assert abs(float(lse[bi, hi, r]) - float(wl[0])) <= 1e-3 * max(1.0, abs(float(wl[0])))
     # row 0 attends only to key 0: o[.,.,0] == v[.,.,0] exactly up to bf16 rounding
     assert torch.allclose(o[:, :, 0].float(), v[:, :, 0].float(), atol=1e-2)
+
+
+@pytest.mark.parametrize("w", [16, 5, 32])
+def test_reference_precision_attention_case(P, golden, w):
+    """MIMW_PREC_F32 holds the reference's own 1e-4 (acceptance.cpp:333-355)
+    for the degeneration case, and matches the restated oracle at other windows."""
+    case = golden["attention_degeneration"]
+    xs = case_inputs(case)
+    q, k, v = xs["q"], xs["k2"], xs["v2"]
+    o, lse = P.oracle_attention(q, k, v, w, 0.25, with_lse=True, precision=P.PREC_F32)
+    want, wl = oracle.oracle_attention(q, k, v, w, 0.25, with_lse=True)
+    assert oracle.rel_error(o, want) <= 1e-5
+    assert np.abs(lse - wl).max() <= 1e-5
+    if w == 16:
+        assert oracle.rel_error(o, case_outputs(case)["o"]) <= case["tolerance"]  # 1e-4
+        got = P.run_oracle("attention", {"q": q, "k": k, "v": v}, {"w": 16, "scale": 0.25},
+                           precision=P.PREC_F32)["o"]
+        assert oracle.rel_error(got, case_outputs(case)["o"]) <= case["tolerance"]

@@ -86,3 +86,18 @@ def test_device_full_oracle_small(P):
     wo, wl = oracle.oracle_simplicial_attention(*(x[0] for x in xs), w1, w2, 0.1)
     assert oracle.rel_error(o[0].float().cpu().numpy(), wo) <= TOL
     assert oracle.rel_error(lse[0].cpu().numpy(), wl) <= TOL
+
+
+def test_reference_precision_case(P, golden):
+    """MIMW_PREC_F32: the reference case at its own 1e-3 (simplicial_attention.case)."""
+    case = golden["simplicial_attention"]
+    xs = case_inputs(case)
+    sc = case["scalars"]
+    o, lse = P.oracle_simplicial_attention(xs["q"], xs["k1"], xs["v1"], xs["k2"], xs["v2"],
+                                           int(sc["w1"]), int(sc["w2"]), sc["scale"],
+                                           precision=P.PREC_F32)
+    outs = case_outputs(case)
+    assert oracle.rel_error(o, outs["o"]) <= case["tolerance"]
+    assert oracle.rel_error(lse, outs["lse"]) <= case["tolerance"]
+    out = P.run_oracle("simplicial_attention", xs, sc, precision=P.PREC_F32)
+    assert oracle.rel_error(out["o"], outs["o"]) <= case["tolerance"]

@@ -105,6 +105,21 @@ __device__ __forceinline__ void tma_reduce_add_3d(const void *tmap, uint32_t src
       : "memory");
 }
 
+#ifdef MIMW_BWD_TRACE
+// per-warp cycle accounting of the first 4 CTAs (tools/bwd_trace.py):
+// [cta][warp][8] = role-specific wait buckets, [7] = total
+__device__ unsigned long long g_bwd_trace[4 * 16 * 8];
+#define TR_DECL unsigned long long tr_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; const long long tr_t0 = clock64();
+#define TR(i, stmt) do { const long long t_ = clock64(); stmt; tr_[i] += clock64() - t_; } while (0)
+#define TR_END \
+  if (blockIdx.x < 4 && lane == 0) { tr_[7] = clock64() - tr_t0; \
+    for (int e_ = 0; e_ < 8; ++e_) g_bwd_trace[(blockIdx.x * 16 + warp) * 8 + e_] = tr_[e_]; }
+#else
+#define TR_DECL
+#define TR(i, stmt) stmt
+#define TR_END
+#endif
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -164,6 +179,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  TR_DECL
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -176,7 +192,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       for (int t = 0; t < n; ++t) {
         const int s = t % NST;
         const int i = q_tile(t);
-        mbar_wait(ld_empty(s), ((t / NST) & 1) ^ 1, 1);
+        TR(1, mbar_wait(ld_empty(s), ((t / NST) & 1) ^ 1, 1));
         mbar_arrive_expect_tx(ld_full(s), 2 * QT_BYTES);
         for (int h = 0; h < 2; ++h) {
           tma_load_3d(sbase + SM_Q + s * QT_BYTES + h * QPANEL, &tmQ, ld_full(s), 64 * h, i * BQ, bh);
@@ -192,7 +208,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       constexpr uint32_t LO_K = (16u >> 4) << 16;                       // K-major: LBO unused
       auto issue_S = [&](int t, bool dp) {
         const int st = t % NST;
-        if (!dp) mbar_wait(ld_full(st), (t / NST) & 1, 2);
+        if (!dp) TR(1, mbar_wait(ld_full(st), (t / NST) & 1, 2));
         tc_fence_after();
         const uint32_t a0 = (sbase + (dp ? SM_V : SM_K)) >> 4;
         const uint32_t b0 = (sbase + (dp ? SM_DO : SM_Q) + st * QT_BYTES) >> 4;
@@ -218,15 +234,15 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         const int s = t & 1;      // S^T buffer and dS^T smem buffer
         const int st = t % NST;   // Q / dO stage
         if (t + 1 < n) {
-          mbar_wait(dp_free, t & 1, 4);  // dP^T_t is in the softmax warps' registers
+          TR(2, mbar_wait(dp_free, t & 1, 4));  // dP^T_t is in the softmax warps' registers
           issue_S(t + 1, true);
           if (elect_one()) mma_commit(s_full);
           __syncwarp();
         }
-        mbar_wait(p_full, t & 1, 5);
+        TR(3, mbar_wait(p_full, t & 1, 5));
         tc_fence_after();
         if (t >= 1) {
-          mbar_wait(dq_free, (t - 1) & 1, 6);  // dQ^T_{t-1} drained
+          TR(4, mbar_wait(dq_free, (t - 1) & 1, 6));  // dQ^T_{t-1} drained
           tc_fence_after();
         }
         if (elect_one()) {
@@ -285,7 +301,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         const float *src = ctid < 64 ? p.lse2 : p.dvec;
         pre = __ldg(src + ((size_t)bh * p.nq + q_tile(t + 1)) * BQ + (ctid & 63));
       }
-      mbar_wait(s_full, t & 1, 7);
+      TR(1, mbar_wait(s_full, t & 1, 7));
       tc_fence_after();
       uint32_t sv[32], dp[32];
       const uint32_t t_s = tmem + t_lane + TM_S + 64 * s + 32 * ch;
@@ -324,7 +340,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       tmem_st_32x32b_x16(t_s + 16, dk2);
       // dS^T half-row -> smem buffer s (B operand of dQ^T, MN-major SW128:
       // 16-B chunk c of row r at c ^ (r & 7)); buffer s was last read by dQ_{t-2}
-      if (t >= 2) mbar_wait(ds_free(s), ((t - 2) >> 1) & 1, 9);
+      if (t >= 2) TR(2, mbar_wait(ds_free(s), ((t - 2) >> 1) & 1, 9));
       const uint32_t rbase = sbase + SM_DS + s * BKV * 128 + krow * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -336,7 +352,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
       if (ctid < 128) *reinterpret_cast<float *>(smem + SM_LD + ((t + 1) & 1) * 512 + ctid * 4) = pre;
-      named_bar_sync(1, 256);  // next step's lse2 / D visible; this step's reads done
+      TR(3, named_bar_sync(1, 256));  // next step's lse2 / D visible; this step's reads done
     }
     // ---------------- epilogue: dV, dK (x scale) -> bf16 HBM ----------------
     if (n > 0) {
@@ -378,7 +394,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     const uint32_t stage = sbase + SM_DQ + dd * 8192;
     for (int t = 0; t < n; ++t) {
       const int i = q_tile(t);
-      mbar_wait(dq_full, t & 1, 11);
+      TR(1, mbar_wait(dq_full, t & 1, 11));
       tc_fence_after();
       uint32_t v[64];
       tmem_ld_32x32b_x32(tmem + t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
@@ -388,7 +404,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(dq_free);
-        bulk_wait_read<0>();  // the previous reduce has read the staging buffer
+        TR(2, bulk_wait_read<0>());  // the previous reduce has read the staging buffer
       }
       __syncwarp();
       // two boxes [32 d][32 queries] f32, SWIZZLE_128B: chunk c of row r at c ^ (r & 7)
@@ -412,6 +428,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     __syncwarp();
   }
 
+  TR_END
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -551,3 +568,16 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
 }
 
 }  // namespace mimw
+
+// Debug hook (not in the public header): per-warp cycle buckets of the first
+// 4 CTAs when built with -DMIMW_BWD_TRACE (tools/bwd_trace.py).
+extern "C" int mimw_b200_debug_bwd_trace(unsigned long long *host, int n) {
+#ifdef MIMW_BWD_TRACE
+  if (n > 4 * 16 * 8) n = 4 * 16 * 8;
+  return cudaMemcpyFromSymbol(host, mimw::g_bwd_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 3;
+#else
+  (void)host;
+  (void)n;
+  return 2;
+#endif
+}

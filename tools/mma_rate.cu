@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128, 1) k(long long *out, int iters) {
     if (acc == 12345) out[1000] = acc;
   }
   if (threadIdx.x == 0) {
-    constexpr int N = MODE == 2 ? 256 : (MODE == 3 ? 64 : 128);
+    constexpr int N = MODE == 2 ? 256 : ((MODE == 3 || MODE == 11 || MODE == 12) ? 64 : 128);
     constexpr bool BMN = MODE == 4 || MODE == 5 || MODE == 7 || MODE == 8 || MODE == 10;
     const uint32_t id = idesc_bf16(128, N, 0, BMN ? 1 : 0);
     long long t0 = clock64();
@@ -61,6 +61,8 @@ __global__ void __launch_bounds__(128, 1) k(long long *out, int iters) {
         const uint64_t b = BMN ? smem_desc_sw128(sb + 32768 + (i & 7) * 2048, 16384, 1024)
                                : smem_desc_sw128(sb + 32768 + (i & 3) * 32, 16, 1024);
         if (MODE == 1 || MODE == 4 || MODE == 8 || MODE == 10) mma_f16_ts<1>(tm + 256, tm + (i & 7) * 8, b, id, 1);
+        else if (MODE == 11) mma_f16_ss<1>(tm + (i & 1) * 64, a, b, id, 1);     // two independent N64 chains
+        else if (MODE == 12) mma_f16_ss<1>(tm + (i & 3) * 64, a, b, id, 1);     // four independent N64 chains
         else mma_f16_ss<1>(tm, a, b, id, 1);
       }
       mma_commit(smem_u32(&bar));
@@ -97,5 +99,7 @@ int main() {
   run(k<8>, "TS-MN + 3 warps LDTM", 64);
   run(k<9>, "SS + 3 warps LDTM", 64);
   run(k<10>, "TS-MN + LDTM+STTM", 64);
+  run(k<11>, "SS N64 x2 chains", 32);
+  run(k<12>, "SS N64 x4 chains", 32);
   return 0;
 }

@@ -123,8 +123,16 @@ def dist_init(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
+        # MIMW_BENCH_BACKEND=gloo runs every rank on the visible GPU(s) modulo
+        # their count: a functional check of the multi-rank paths on a 1-GPU box
+        # (numbers from such a run are not scaling measurements)
+        backend = os.environ.get("MIMW_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, ws, local

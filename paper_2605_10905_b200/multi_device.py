@@ -267,7 +267,13 @@ class AllGatherGemm:
     def b_local(self):
         return self._view(self.layouts[self.rank]["b"], (self.k_splits[self.rank], self.n))
 
-    def __call__(self, out=None, gather_output: bool = False, stream=None):
+    def __call__(self, out=None, gather_output: bool = False, stream=None,
+                 device_barrier: bool = True):
+        """One fused gather+GEMM step; returns this rank's C rows (or all of C
+        with ``gather_output``).  ``device_barrier=False`` skips the kernel's
+        entry/exit barrier: the caller then orders the ranks itself (e.g. a
+        host barrier before and after), as on one GPU shared by several
+        processes, where the ranks' kernels cannot be co-resident."""
         import torch
         if self._ws is None:
             self._ws = torch.empty(self.ws_bytes + 1024, dtype=torch.uint8, device=self.device)
@@ -279,8 +285,10 @@ class AllGatherGemm:
         wp = (self._ws.data_ptr() + 1023) & ~1023
         multi_device_gemm(self.rank, self.world, self.a_ptrs, self.b_ptrs, self.k_splits, self.m,
                           self.n, self.row0, self.nrows, out.data_ptr(), self.n, wp,
-                          self._ws.numel() - (wp - self._ws.data_ptr()), pads=self.pad_ptrs,
-                          epoch=self.epoch, comm_pairs=self.comm_pairs, stream=stream)
+                          self._ws.numel() - (wp - self._ws.data_ptr()),
+                          pads=self.pad_ptrs if device_barrier else None,
+                          epoch=self.epoch if device_barrier else 0, comm_pairs=self.comm_pairs,
+                          stream=stream)
         if not gather_output:
             return out
         from .shard import all_gather_rows

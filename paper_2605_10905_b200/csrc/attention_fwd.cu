@@ -170,7 +170,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     if (lane == 0) {
       int slot = 0;
       uint32_t slot_phase = 0;
-      uint32_t qe_phase = 0;
+      uint32_t qe_phase[2] = {0, 0};  // per Q tile: a tile beyond seq is neither loaded nor released
       int it = blockIdx.x;
       for (int n = 0;; ++n) {
         // publish the work item (or -1) to the consumers
@@ -188,13 +188,17 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         if (r0 + BQ >= p.seq) hi1 = hi0;  // Q tile 1 entirely beyond seq: no extra tile
         const int lo = min(lo0, lo1), hi = max(hi0, hi1);
         for (int h = 0; h < 2; ++h) {
-          mbar_wait(q_empty(h), qe_phase ^ 1, 10);
+          // Q tile 1 beyond seq: skipped on every side (no load, no q_full
+          // wait, no release), so q_empty(h) completes exactly once per load
+          // and can never run two phases ahead of this wait
+          if (h == 1 && r0 + BQ >= p.seq) continue;
+          mbar_wait(q_empty(h), qe_phase[h] ^ 1, 10);
           mbar_arrive_expect_tx(q_full(h), TILE_BYTES);
           const uint32_t dq = sbase + SMEM_Q + h * TILE_BYTES;
           tma_load_3d(dq, &tmQ, q_full(h), 0, r0 + h * BQ, bh);
           tma_load_3d(dq + HALF_BYTES, &tmQ, q_full(h), 64, r0 + h * BQ, bh);
+          qe_phase[h] ^= 1;
         }
-        qe_phase ^= 1;
         // next item: claimed now so the consumers never wait on the atomic
         it = atomicAdd(p.work_counter, 1) + (int)gridDim.x;
         for (int j = lo; j <= hi; ++j) {
@@ -217,7 +221,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     // uniform datapath); one elected lane issues tcgen05.mma / commit.
     const bool s_role = warp == 9;
     uint32_t ring = 0;  // K/V ring positions consumed so far (K_j at 2(j-lo), V_j at 2(j-lo)+1)
-    uint32_t q_phase = 0, sf_phase = 0;
+    uint32_t q_phase[2] = {0, 0}, sf_phase = 0;
     uint32_t p_phase0 = 0, p_phase1 = 0;
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t sb = __shfl_sync(0xffffffffu, sbase, 0);
@@ -303,11 +307,12 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       const int lo = min(lo0, lo1), hi = max(hi0, hi1);
       if (s_role) {
         MIMW_TR_BEGIN
-        mbar_wait(q_full(0), q_phase, 21);
-        mbar_wait(q_full(1), q_phase, 22);
+        mbar_wait(q_full(0), q_phase[0], 21);
+        if (has1) mbar_wait(q_full(1), q_phase[1], 22);
         MIMW_TR_END(6)
       }
-      q_phase ^= 1;
+      q_phase[0] ^= 1;
+      if (has1) q_phase[1] ^= 1;
       // Two issuers keep the tensor pipe fed: tcgen05.mma issue blocks at the
       // pipe rate, so while one warp waits on a dependency the other's group
       // is already queued.  Warp 9 issues every S = Q K^T (and releases K
@@ -368,10 +373,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       kv_range(rt, p, lo, hi);
       float m_used = -INFINITY;  // log2-domain max the exponentials are taken against
       float l = 0.f;
-      if (!tile_live) {
-        if (lane == 0) mbar_arrive(q_empty(h));
-        continue;
-      }
+      if (!tile_live) continue;  // tile beyond seq: never loaded, nothing to release
       for (int j = lo; j <= hi; ++j) {
 #ifdef MIMW_FA_TRACE
         const long long tr0 = clock64();

@@ -1,0 +1,35 @@
+"""A/B timing of the FA forward between two builds of the library on one box:
+    python tools/fa_ab.py <lib_a.so> <lib_b.so> [rounds]"""
+import sys
+import os
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_10905_b200 as P  # noqa: E402
+
+libs = sys.argv[1:3]
+rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+q, k, v = ((torch.rand((4, 32, 8192, 128), device="cuda") * 2 - 1).bfloat16() for _ in range(3))
+flop = 4.0 * 128 * 128 * 8192 * 8192 / 2
+handles = []
+for path in libs:
+    P._lib = None
+    P.LIB_PATH = path
+    handles.append(P.lib())
+import time
+for r in range(rounds):
+    order = list(zip(libs, handles)) if r % 2 == 0 else list(zip(libs, handles))[::-1]
+    for path, L in order:
+        time.sleep(1.5)  # let the power state settle between measurements
+        P._lib = L
+        o, lse = P.attention_fwd(q, k, v)
+        for _ in range(3):
+            P.attention_fwd(q, k, v, out=o, lse=lse)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            P.attention_fwd(q, k, v, out=o, lse=lse)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        print(r, os.path.basename(path), round(flop / ms / 1e9, 1), flush=True)

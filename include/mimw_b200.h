@@ -193,7 +193,7 @@ int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o
  * backward); oracle: the f64 restatement orc_attention_bwd in oracle/oracle.c.
  * q, k, v, o, dout, dq, dk, dv bf16 [batch, heads, seq, 128] contiguous; lse
  * fp32 [batch, heads, seq] (natural log, as written by mimw_b200_attention_fwd).
- * seq % 4 == 0.  KV-stationary tcgen05 kernel (key-major S^T / dP^T so P^T and
+ * Any seq >= 0.  KV-stationary tcgen05 kernel (key-major S^T / dP^T so P^T and
  * dS^T feed the dV / dK MMAs from TMEM), dQ accumulated by TMA reduce-add. */
 int mimw_b200_attention_bwd(const void *q, const void *k, const void *v, const void *o,
                             const void *dout, const float *lse, void *dq, void *dk, void *dv,

@@ -470,14 +470,14 @@ __global__ void attention_bwd_prep(const __nv_bfloat16 *o, const __nv_bfloat16 *
 }
 
 // dQ[bh, s, d] = bf16(scale * dQacc^T[bh, d, s]) through 32 x 32 smem tiles
-__global__ void attention_bwd_dq(const float *acc, __nv_bfloat16 *dq, int seq, float scale) {
+__global__ void attention_bwd_dq(const float *acc, __nv_bfloat16 *dq, int seq, int ld, float scale) {
   __shared__ float tile[32][33];
   const int b = blockIdx.z;
   const int s0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
-  const float *src = acc + (size_t)b * D * seq;
+  const float *src = acc + (size_t)b * D * ld;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int s = s0 + threadIdx.x;
-    tile[r][threadIdx.x] = s < seq ? src[(size_t)(d0 + r) * seq + s] : 0.f;
+    tile[r][threadIdx.x] = s < seq ? src[(size_t)(d0 + r) * ld + s] : 0.f;
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -495,8 +495,10 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
   const int nq = (seq + BQ - 1) / BQ;
   const int nkv = (seq + BKV - 1) / BKV;
   const int npad = nq * BQ;
-  // workspace: dQ accumulator [bh, 128, seq] f32, lse2 / D [bh, npad] f32
-  const size_t acc_bytes = (size_t)bh * D * seq * 4;
+  // workspace: dQ accumulator [bh, 128, npad] f32 (rows padded to the query
+  // tile so the TMA row stride is a 256-B multiple for any seq), lse2 / D
+  // [bh, npad] f32
+  const size_t acc_bytes = (size_t)bh * D * npad * 4;
   const size_t vec_bytes = (size_t)bh * npad * 4;
   // stream-ordered scratch from the device's default pool, which is told to
   // keep its memory (the default release threshold of 0 hands the ~0.8 GB
@@ -537,7 +539,7 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
                                   BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     CUtensorMap tV = make_tmap_3d(a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, seq, ubh, D, (uint64_t)seq * D, 64,
                                   BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-    CUtensorMap tDQ = make_tmap_3d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, seq, D, ubh, seq, (uint64_t)D * seq,
+    CUtensorMap tDQ = make_tmap_3d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, seq, D, ubh, npad, (uint64_t)D * npad,
                                    32, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     BwdParams p;
     p.bh = bh;
@@ -560,7 +562,7 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
   }
   if (e == cudaSuccess) {
     attention_bwd_dq<<<dim3((seq + 31) / 32, D / 32, bh), dim3(32, 8), 0, stream>>>(
-        acc, static_cast<__nv_bfloat16 *>(a.dq), seq, (float)a.scale);
+        acc, static_cast<__nv_bfloat16 *>(a.dq), seq, npad, (float)a.scale);
     e = cudaGetLastError();
   }
   cudaError_t e2 = cudaFreeAsync(ws, stream);

@@ -533,7 +533,6 @@ int mimw_b200_attention_bwd(const void *q, const void *k, const void *v, const v
     require(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
              (uintptr_t)dk | (uintptr_t)dv) % 16 == 0,
             MIMW_ERR_UNSUPPORTED, "tensors must be 16-byte aligned");
-    require(seq % 4 == 0, MIMW_ERR_UNSUPPORTED, "seq must be a multiple of 4 (16-byte dQ accumulator rows)");
     require_sm100();
     mimw::AttnBwdArgs a{};
     a.q = q;

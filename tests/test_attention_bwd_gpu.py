@@ -115,5 +115,5 @@ def test_backward_arguments(P):
     import torch
     q = torch.zeros((1, 1, 130, 128), device="cuda", dtype=torch.bfloat16)
     lse = torch.zeros((1, 1, 130), device="cuda")
-    with pytest.raises(P.MimwError):  # seq % 4
-        P.attention_bwd(q, q, q, q, q, lse)
+    with pytest.raises(P.MimwError):  # negative window
+        P.attention_bwd(q, q, q, q, q, lse, window=-3)

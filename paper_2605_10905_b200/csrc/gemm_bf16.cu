@@ -32,7 +32,9 @@
 #include "tma_host.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace mimw {
 
@@ -58,7 +60,7 @@ struct Cfg {
   static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF;
   static constexpr int COMM_EXTRA = GATHER ? 16384 : 0;        // distributed comm warp's buffer
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES + EPI_BYTES + COMM_EXTRA;
-  static constexpr int BAR_BYTES = 256;                        // pipeline barriers + TMEM slot
+  static constexpr int BAR_BYTES = 384;                        // pipeline barriers + TMEM slot + CLC ring
   static constexpr int COMM_BAR_BYTES = 8 * 24 + 32;           // all-gather comm barriers + mailboxes
   static constexpr int SMEM = BAR_OFF + BAR_BYTES + COMM_BAR_BYTES + 1024;  // + align slack
   static constexpr uint32_t IDESC = idesc_bf16(BM_CTA * CG, BN, 0, B_MN ? 1 : 0);
@@ -105,36 +107,51 @@ using Sched = SchedT<1>;
 // Grouped (MoE) problem: Y_e[m_e, N] = X[row_off_e : row_off_e + m_e, K] . W_e
 // for e < n_groups.  X rows are packed by group; W is one [G, K, N] (or
 // [G, N, K]) tensor read through a 3-D tensor map; every group has its own
-// Y tensor map whose row extent m_e clips the tail tile's store.  Tile order:
-// groups in turn, N-tiles outer, M-tiles inner, so the CTA pairs working on
-// one weight panel W_e[:, n-tile] run at the same time and share it in L2.
+// Y tensor map whose row extent m_e clips the tail tile's store.
+// Tile order: the non-empty groups are visited in `order` and cut into chunks
+// of consecutive slots; inside a chunk, N-tiles outer, then (group, M-tile),
+// so the CTA pairs working on one weight panel W_e[:, n-tile] run at the same
+// time and share it in L2, and a chunk that mixes heavy and light groups
+// keeps compute-bound and weight-streaming tiles running side by side.
+// One group per chunk is plain "groups in turn".
 constexpr int MAX_GROUPS = 128;
 struct GroupedSched {
   static constexpr bool kGrouped = true;
   static constexpr bool kGather = false;
   static constexpr int kPairs = 1;
   CUtensorMap y[MAX_GROUPS];
-  int tile_off[MAX_GROUPS + 1];  // prefix sum of m_tiles(e) * num_n
-  int row_off[MAX_GROUPS];       // first row of group e in X / Y
-  int rows[MAX_GROUPS];          // m_e
-  int n_groups, num_n, bm;       // bm = rows per cluster tile (128 * CG)
-  int swap;                      // tail tiles (< bm rows) use swapped operands (CG == 2)
-  __device__ __forceinline__ int num_tiles() const { return tile_off[n_groups]; }
+  int order[MAX_GROUPS];           // slot -> group
+  int mt_pref[MAX_GROUPS + 1];     // prefix over slots of m_tiles(group)
+  int chunk_off[MAX_GROUPS + 1];   // first tile of chunk c
+  int chunk_slot[MAX_GROUPS + 1];  // first slot of chunk c
+  int row_off[MAX_GROUPS];         // first row of group e in X / Y
+  int rows[MAX_GROUPS];            // m_e
+  int n_chunks, num_n, bm;         // bm = rows per cluster tile (128 * CG)
+  int swap;                        // tail tiles (< bm rows) use swapped operands (CG == 2)
+  int clc;                         // tiles dispatched by cluster launch control (grid = one cluster per tile)
+  __device__ __forceinline__ int num_tiles() const { return chunk_off[n_chunks]; }
   __device__ __forceinline__ TileCoord decode(int t) const {
-    int lo = 0, hi = n_groups - 1;  // last e with tile_off[e] <= t
+    int lo = 0, hi = n_chunks - 1;  // last chunk with chunk_off[c] <= t
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (tile_off[mid] <= t) lo = mid; else hi = mid - 1;
+      const int mid = (lo + hi + 1) >> 1;
+      if (chunk_off[mid] <= t) lo = mid; else hi = mid - 1;
     }
-    const int e = lo;
-    const int r = t - tile_off[e];
+    const int s0 = chunk_slot[lo], s1 = chunk_slot[lo + 1];
+    const int per_n = mt_pref[s1] - mt_pref[s0];
+    const int r = t - chunk_off[lo];
+    const int q = mt_pref[s0] + r % per_n;
+    int a = s0, b = s1 - 1;  // last slot with mt_pref[slot] <= q (slots are non-empty)
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (mt_pref[mid] <= q) a = mid; else b = mid - 1;
+    }
+    const int e = order[a];
     const int full = rows[e] / bm;
     const int tail = rows[e] - full * bm;
-    const int mtiles = full + (tail > 0);
     TileCoord c;
     c.e = e;
-    c.mt = r % mtiles;
-    c.nt = r / mtiles;
+    c.mt = q - mt_pref[a];
+    c.nt = r / per_n;
     c.row_base = row_off[e];
     c.rows = rows[e];
     c.swap_n = (swap && c.mt == full && tail > 0) ? ((tail + 31) & ~31) : 0;
@@ -171,6 +188,15 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   auto tfull_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + a); };
   auto tempty_bar = [&](int a) { return bar_base + 8 * (2 * C::STAGES + ACC_STAGES + a); };
   const uint32_t tmem_slot = bar_base + 8 * (2 * C::STAGES + 2 * ACC_STAGES);
+  // CLC response ring (gemm_clc.mimw's clc_producer / clc_consumer): slot s =
+  // 16-byte response + full barrier (completed by the response bytes) + empty
+  // barrier on the pair leader (released by every consumer of both CTAs)
+  constexpr int CLC_SLOTS = 4;
+  constexpr uint32_t CLC_CONSUMERS = CG * (1 + EPI_WARPS) + 1;  // producers, epilogue warps, MMA warp
+  auto clc_resp = [&](int s) { return bar_base + 256 + 16 * s; };
+  auto clc_full = [&](int s) { return bar_base + 256 + 16 * CLC_SLOTS + 8 * s; };
+  auto clc_empty = [&](int s) { return bar_base + 256 + 24 * CLC_SLOTS + 8 * s; };
+  static_assert(256 + 32 * CLC_SLOTS <= C::BAR_BYTES, "CLC ring");
   uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * C::STAGES + 2 * ACC_STAGES));
 
   const int warp = threadIdx.x / 32;
@@ -183,6 +209,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   int nclusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
   const int num_tiles = sched.num_tiles();
   int num_k = (K + BK - 1) / BK;
+  bool clc = false;
+  if constexpr (GROUPED) clc = sched.clc != 0;
   bool comm = false;  // all-gather GEMM: the low cluster ids are comm pairs
   if constexpr (Prob::kGather) {
     static_assert(CG == 2 && B_MN && PAIRS == 1, "all-gather GEMM: 2-CTA, B as [K, N]");
@@ -204,6 +232,11 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), EPI_WARPS * CG);
     }
+    if (clc)
+      for (int s = 0; s < CLC_SLOTS; ++s) {
+        mbar_init(clc_full(s), 1);
+        mbar_init(clc_empty(s), CLC_CONSUMERS);
+      }
     if constexpr (Prob::kGather)
       for (int i = 0; i < 8; ++i)  // comm mailboxes
         st_release_cta_shared(bar_base + C::BAR_BYTES + 8 * COMM_MAX_BUFS + 4 * i, 0u);
@@ -214,6 +247,34 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+
+  // Next tile after tile t (use index u): static striding, or the u-th CLC
+  // response (the cancelled cluster's tile; num_tiles once the grid is
+  // exhausted).  Every consumer reads every response, `arrive` once per warp.
+  auto next_tile = [&](int t, int u, bool arrive) -> int {
+    if (!clc) return t + nclusters;
+    const int slot = u % CLC_SLOTS;
+    mbar_wait(clc_full(slot), (uint32_t)(u / CLC_SLOTS) & 1, 12);
+    const int x = clc_query(clc_resp(slot));
+    if (arrive) {
+      if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(clc_empty(slot), my_leader));
+      else mbar_arrive(clc_empty(slot));
+    }
+    return x < 0 ? num_tiles : x / (CG * PAIRS);
+  };
+  // Producer, at the start of tile u: the pair leader asks for tile u + 1
+  // (multicast to both CTAs); each CTA arms its own full barrier for it.
+  auto clc_request = [&](int u) {
+    const int slot = u % CLC_SLOTS;
+    if (leader) {
+      mbar_wait_cluster(clc_empty(slot), ((uint32_t)(u / CLC_SLOTS) & 1) ^ 1, 13);
+      mbar_arrive_expect_tx(clc_full(slot), 16);
+      if constexpr (CG == 2) clc_try_cancel_multicast(clc_resp(slot), clc_full(slot));
+      else clc_try_cancel(clc_resp(slot), clc_full(slot));
+    } else {
+      mbar_arrive_expect_tx(clc_full(slot), 16);
+    }
+  };
 
   if (comm) {
     if constexpr (Prob::kGather)
@@ -226,7 +287,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full_target0 = (CG == 2) ? map_to_rank(full_bar(0), my_leader) : full_bar(0);
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, true)) {
+        if (clc) clc_request(u);
         const TileCoord tc = sched.decode(t);
         // swapped tail tile: this CTA stages rows [swap_n/2 * rank, +swap_n/2) of the
         // group's tail as the MMA's B operand (same 128-row box; extra rows unused)
@@ -322,7 +384,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, lane_id() == 0)) {
         int swap_n = 0;
         if constexpr (GROUPED) swap_n = sched.decode(t).swap_n;
         // swapped tail: A = W^T (the B slot, MN-major for [G,K,N]), B = X rows (the A slot)
@@ -392,7 +454,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     int acc = 0;
     uint32_t acc_phase = 0;
     int buf = 0;
-    for (int t = cluster; t < num_tiles; t += nclusters) {
+    for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, lane == 0)) {
       const TileCoord tc = sched.decode(t);
       const int row0 = (tc.mt * PAIRS + pair) * BM_CTA * CG + (int)rank * BM_CTA + q * 32;  // C-map row
       const int col0 = tc.nt * BN;
@@ -544,6 +606,8 @@ cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CU
   clusters -= comm_clusters;
   if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
   if (clusters > tiles) clusters = tiles;
+  if constexpr (Prob::kGrouped)
+    if (prob_in.clc) clusters = tiles;  // CLC: one cluster per tile, running clusters cancel the rest
   if (clusters <= 0 && tiles > 0) return cudaErrorInvalidConfiguration;
   if (clusters < 0) clusters = 0;
   if (clusters + comm_clusters == 0) return cudaSuccess;
@@ -598,6 +662,31 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
                                        g.max_clusters, stream);
 }
 
+// Slot order of the non-empty groups for chunks of `chunk` groups: groups
+// sorted by rows, dealt to the chunks in a snake (chunk 0 gets the heaviest and
+// the lightest, ...) so every chunk mixes compute-bound full tiles with
+// weight-streaming light groups.  chunk <= 1 keeps the natural order.
+std::vector<int> grouped_order(const std::vector<int> &live, const int *rows, int chunk) {
+  static const int sort_env = getenv("MIMW_MOE_SORT") ? atoi(getenv("MIMW_MOE_SORT")) : 0;  // A/B knob
+  if (chunk <= 1 && sort_env != 0) {
+    std::vector<int> v = live;
+    std::stable_sort(v.begin(), v.end(), [&](int x, int y) { return sort_env > 0 ? rows[x] > rows[y] : rows[x] < rows[y]; });
+    return v;
+  }
+  if (chunk <= 1) return live;
+  std::vector<int> by_rows = live;
+  std::stable_sort(by_rows.begin(), by_rows.end(), [&](int a, int b) { return rows[a] > rows[b]; });
+  const int nc = (int)((live.size() + chunk - 1) / chunk);
+  std::vector<std::vector<int>> chunks((size_t)nc);
+  for (size_t i = 0; i < by_rows.size(); ++i) {
+    const int round = (int)(i / nc), pos = (int)(i % nc);
+    chunks[(size_t)((round & 1) ? nc - 1 - pos : pos)].push_back(by_rows[i]);
+  }
+  std::vector<int> out;
+  for (auto &c : chunks) out.insert(out.end(), c.begin(), c.end());
+  return out;
+}
+
 // One launch per chunk of <= MAX_GROUPS groups (the Y maps travel in the
 // kernel's parameter block).
 template <int CG, bool B_MN>
@@ -606,7 +695,10 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
   const int64_t total_rows = g.m_offsets[g.n_groups];
   CUtensorMap tA = make_tmap_2d(g.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, total_rows, g.k, g.k, BK,
                                 BM_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
-  auto *gs = new GroupedSched;  // ~18 KB: keep it off the host stack
+  auto *gs = new GroupedSched;  // ~20 KB: keep it off the host stack
+  static const int chunk_env = getenv("MIMW_MOE_CHUNK") ? atoi(getenv("MIMW_MOE_CHUNK")) : -1;  // A/B knob
+  const int chunk = chunk_env >= 0 ? chunk_env : 1;
+  static const int clc_env = getenv("MIMW_GEMM_CLC") ? atoi(getenv("MIMW_GEMM_CLC")) : 1;  // A/B knob
   cudaError_t err = cudaSuccess;
   for (int64_t g0 = 0; g0 < g.n_groups && err == cudaSuccess; g0 += MAX_GROUPS) {
     const int cnt = (int)std::min<int64_t>(MAX_GROUPS, g.n_groups - g0);
@@ -616,28 +708,46 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
                           : make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, cnt,
                                          g.k, g.k * g.n, BK, C::NB_CTA, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     std::memset(gs, 0, sizeof(GroupedSched));
-    gs->n_groups = cnt;
     gs->num_n = (int)((g.n + BN - 1) / BN);
     gs->bm = BM_CTA * CG;
     gs->swap = (CG == 2 && g.swap_tails) ? 1 : 0;
-    int tiles = 0;
+    gs->clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;  // max_clusters bounds a persistent grid
     int first_live = -1;
+    std::vector<int> live;
     for (int i = 0; i < cnt; ++i) {
       const int64_t r0 = g.m_offsets[g0 + i], r1 = g.m_offsets[g0 + i + 1];
-      gs->tile_off[i] = tiles;
       gs->row_off[i] = (int)r0;
       gs->rows[i] = (int)(r1 - r0);
-      tiles += (int)((r1 - r0 + gs->bm - 1) / gs->bm) * gs->num_n;
       if (r1 > r0) {
         gs->y[i] = make_c_map<__nv_bfloat16>(static_cast<char *>(g.y) + (size_t)r0 * g.n * 2,
                                              r1 - r0, g.n, g.n);
         if (first_live < 0) first_live = i;
+        live.push_back(i);
       }
     }
-    gs->tile_off[cnt] = tiles;
-    if (tiles == 0) continue;
+    if (live.empty()) continue;
     for (int i = 0; i < cnt; ++i)
       if (gs->rows[i] == 0) gs->y[i] = gs->y[first_live];  // never stored through
+    const std::vector<int> order = grouped_order(live, gs->rows, chunk);
+    const int per_chunk = std::max(1, chunk);
+    int tiles = 0, ns = 0;
+    gs->n_chunks = 0;
+    gs->mt_pref[0] = 0;
+    for (size_t s0 = 0; s0 < order.size(); s0 += per_chunk) {
+      gs->chunk_off[gs->n_chunks] = tiles;
+      gs->chunk_slot[gs->n_chunks] = ns;
+      int mts = 0;
+      for (size_t j = s0; j < std::min(order.size(), s0 + per_chunk); ++j, ++ns) {
+        const int e = order[j];
+        gs->order[ns] = e;
+        mts += (gs->rows[e] + gs->bm - 1) / gs->bm;
+        gs->mt_pref[ns + 1] = gs->mt_pref[ns] + (gs->rows[e] + gs->bm - 1) / gs->bm;
+      }
+      tiles += mts * gs->num_n;
+      ++gs->n_chunks;
+    }
+    gs->chunk_off[gs->n_chunks] = tiles;
+    gs->chunk_slot[gs->n_chunks] = ns;
     err = launch_kernel<CG, B_MN, __nv_bfloat16>(tA, tB, gs->y[first_live], (int)g.n, (int)g.k, *gs,
                                                  tiles, g.max_clusters, stream);
   }

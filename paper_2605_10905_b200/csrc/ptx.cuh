@@ -183,6 +183,47 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity,
 }
 
 // ---------------------------------------------------------------------------
+// Cluster launch control (the reference's CLC producer/consumer,
+// sim.cpp:761-781,1213-1286; 16-byte response): try_cancel asks
+// the hardware for a cluster of this grid that has not been launched yet and,
+// if one is cancelled, the running cluster does its work instead.  The
+// response lands in shared memory with complete_tx on an mbarrier (16 bytes).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void clc_try_cancel(uint32_t resp, uint32_t bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+          resp),
+      "r"(bar)
+      : "memory");
+}
+
+// Same, response written to the same offset in every CTA of the cluster and
+// complete_tx signalled on each CTA's mbarrier at `bar`'s offset.
+__device__ __forceinline__ void clc_try_cancel_multicast(uint32_t resp, uint32_t bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128 "
+      "[%0], [%1];" ::"r"(resp),
+      "r"(bar)
+      : "memory");
+}
+
+// Decode a response: returns the cancelled cluster's first CTA id (x), or -1
+// when nothing was cancelled (the grid is exhausted; issue no further request).
+__device__ __forceinline__ int clc_query(uint32_t resp) {
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
+      "ld.shared.b128 R, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, R;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "r"(resp)
+      : "memory");
+  return ok ? (int)x : -1;
+}
+
+// ---------------------------------------------------------------------------
 // cluster barrier (the reference's cluster_barrier, sim.cpp:1192-1211)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cluster_sync() {

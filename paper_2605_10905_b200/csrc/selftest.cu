@@ -87,6 +87,58 @@ __global__ void __cluster_dims__(2, 1, 1) mbar_selftest_kernel(int *out, const u
   cluster_sync();
 }
 
+
+// CLC exactly-once (the reference's test_clc.cpp:25-92 on the hardware): a
+// grid of `ntiles` clusters in which every running cluster keeps cancelling
+// not-yet-launched clusters and doing their tile, with the same response ring
+// the GEMM uses (2 slots; per slot a full barrier completed by the 16-byte
+// response and an empty barrier on the leader released by every consumer of
+// both CTAs).  count[t] = times tile t was done; ran[c] = tiles cluster c did.
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) clc_selftest_kernel(int *count, int *ran, int spin) {
+  __shared__ alignas(16) uint4 resp[2];
+  __shared__ alignas(8) uint64_t full[2], empty[2];
+  const uint32_t crank = CS > 1 ? cluster_ctarank() : 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 2 * CS);
+    }
+    fence_mbar_init();
+  }
+  if (CS > 1) cluster_sync(); else __syncthreads();
+  const int first = (int)cluster_id_x();
+  if (lane == 0 && warp < 2) {
+    int t = first;
+    for (int u = 0; t >= 0; ++u) {
+      const int slot = u & 1;
+      const uint32_t ph = (uint32_t)(u >> 1) & 1;
+      const uint32_t fb = smem_u32(&full[slot]), rs = smem_u32(&resp[slot]);
+      if (warp == 0) {  // requester, one tile ahead of the response it reads
+        if (crank == 0) {
+          mbar_wait_cluster(smem_u32(&empty[slot]), ph ^ 1, 70);
+          mbar_arrive_expect_tx(fb, 16);
+          if (CS > 1) clc_try_cancel_multicast(rs, fb); else clc_try_cancel(rs, fb);
+          atomicAdd(&count[t], 1);
+          atomicAdd(&ran[first], 1);
+        } else {
+          mbar_arrive_expect_tx(fb, 16);
+        }
+      }
+      const long long t0 = clock64();
+      while (clock64() - t0 < spin) {
+      }
+      mbar_wait(fb, ph, 71);
+      const int x = clc_query(rs);
+      t = x < 0 ? -1 : x / CS;
+      if (CS > 1) mbar_arrive_cluster(map_to_rank(smem_u32(&empty[slot]), 0));
+      else mbar_arrive(smem_u32(&empty[slot]));
+    }
+  }
+  if (CS > 1) cluster_sync(); else __syncthreads();  // no remote arrive targets an exited CTA
+}
+
 }  // namespace
 
 }  // namespace mimw
@@ -107,4 +159,31 @@ extern "C" int mimw_b200_selftest_mbarrier(int *host_out, int n) {
   cudaFree(d);
   cudaFree(src);
   return e == cudaSuccess ? kNumChecks : 3;
+}
+
+// out[0] = tiles not done exactly once, out[1] = clusters that did >= 2 tiles
+// (work was stolen), out[2] = most tiles done by one cluster.  Returns 0, or a
+// CUDA error code.
+extern "C" int mimw_b200_selftest_clc(int ntiles, int cluster, int spin, int *out) {
+  using namespace mimw;
+  if (ntiles <= 0 || !out || (cluster != 1 && cluster != 2)) return -1;
+  int *d = nullptr;
+  if (cudaMalloc(&d, sizeof(int) * 2 * ntiles) != cudaSuccess) return 2;
+  cudaMemset(d, 0, sizeof(int) * 2 * ntiles);
+  if (cluster == 2) clc_selftest_kernel<2><<<2 * ntiles, 64>>>(d, d + ntiles, spin);
+  else clc_selftest_kernel<1><<<ntiles, 64>>>(d, d + ntiles, spin);
+  cudaError_t e = cudaDeviceSynchronize();
+  int *h = new int[2 * (size_t)ntiles];
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(int) * 2 * ntiles, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e == cudaSuccess) {
+    out[0] = out[1] = out[2] = 0;
+    for (int i = 0; i < ntiles; ++i) {
+      out[0] += h[i] != 1;
+      out[1] += h[ntiles + i] >= 2;
+      out[2] = h[ntiles + i] > out[2] ? h[ntiles + i] : out[2];
+    }
+  }
+  delete[] h;
+  return (int)e;
 }

@@ -27,3 +27,21 @@ def test_mbarrier_contract():
     assert n == len(CHECKS)
     failed = [c for c, v in zip(CHECKS, out) if v != 1]
     assert not failed, failed
+
+
+@pytest.mark.parametrize("cluster", [1, 2])
+@pytest.mark.parametrize("ntiles,spin", [(1, 0), (148, 0), (5000, 0), (3000, 20000)])
+def test_clc_exactly_once(cluster, ntiles, spin):
+    """Cluster launch control on the hardware (the reference's test_clc.cpp:
+    25-92: every tile dispatched exactly once, then the -1 sentinel): a grid of
+    ntiles clusters whose running clusters cancel pending ones and do their
+    tiles, with the response ring the grouped GEMM uses."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2605_10905_b200 as P
+    out = (ctypes.c_int * 3)()
+    assert P.lib().mimw_b200_selftest_clc(ntiles, cluster, spin, out) == 0
+    assert out[0] == 0, f"{out[0]} tiles not done exactly once"
+    if ntiles >= 3000:
+        assert out[1] > 0 and out[2] > 1, "no cluster cancelled another (no work stealing)"

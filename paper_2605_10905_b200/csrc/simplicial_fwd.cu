@@ -40,6 +40,7 @@
 #include "tma_host.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mimw {
 
@@ -93,6 +94,7 @@ __device__ unsigned long long g_simp_trace[4 * 12 * 8];
 #define TR_END
 #endif
 
+template <int EMU>  // exponentials per 8 computed by the FMA-pipe polynomial instead of MUFU
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
                       Params p) {
@@ -336,9 +338,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
     bool o_live = false;  // O holds a folded U
     const float sl = p.scale_pos ? p.scale_log2 : 1.f;
     const uint64_t sl2 = f2_pack(sl, sl);
-    for (int n = 0; n < nsteps; ++n) {
-      const int d = n / ntile;
-      const int t = n % ntile;
+    for (int n = 0, d = 0, t = 0; n < nsteps; ++n, t = (t + 1 == ntile) ? 0 : t + 1, d += (t == 0)) {
       const int j1 = i - d;
       const int b = n & 1;
       // ---- S of step n (this group's 64 keys) ----
@@ -356,13 +356,19 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
                              ((lo + t) * BKV + BKV > p.seq) || (i0 + BQ > p.seq) || (i0 < d) || !p.scale_pos;
       const bool live = row_live && j1 >= 0;
       if (need_mask) {
-        const int c_lo = i - p.w2 + 1 - k0;
-        const int c_hi = min(i, p.seq - 1) - k0;
+        // valid columns [c_lo, c_hi] of this group's 64 as a bit mask: one
+        // bit test + select per element instead of two compares + select
+        const int c_lo = max(i - p.w2 + 1 - k0, 0);
+        const int c_hi = min(min(i, p.seq - 1) - k0, 63);
+        uint64_t bits = 0;
+        if (live && c_lo <= c_hi) bits = (~0ull >> (63 - c_hi)) & (~0ull << c_lo);
+        const uint32_t b_lo = (uint32_t)bits, b_hi = (uint32_t)(bits >> 32);
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           float v = __uint_as_float(s[c]);
           if (!p.scale_pos) v *= p.scale_log2;
-          if (!live || c < c_lo || c > c_hi) v = -INFINITY;
+          const uint32_t w = c < 32 ? b_lo : b_hi;
+          if (!(w & (1u << (c & 31)))) v = -INFINITY;
           s[c] = __float_as_uint(v);
         }
       }
@@ -390,7 +396,7 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
         const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), sl2, nm2);
-        const uint64_t p2 = ex2_mufu2(x2);
+        const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
         acc2[e & 3] = f2_add(acc2[e & 3], p2);
         pk[e] = pack_bf16_2(p2);
       }
@@ -527,11 +533,20 @@ cudaError_t simplicial_fwd_launch(const SimplicialArgs &a, cudaStream_t stream) 
   p.nqt = (int)((a.seq + BQ - 1) / BQ);
   p.scale_log2 = (float)(a.scale * 1.4426950408889634);
   p.scale_pos = a.scale > 0 ? 1 : 0;
-  cudaError_t e = cudaFuncSetAttribute(simplicial_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       SMEM_TOTAL);
-  if (e != cudaSuccess) return e;
-  simplicial_fwd_kernel<<<(unsigned)(bh * p.nqt), NUM_THREADS, SMEM_TOTAL, stream>>>(tK2, tV2, p);
-  return cudaGetLastError();
+  static const int emu_env = getenv("MIMW_SIMP_EMU") ? atoi(getenv("MIMW_SIMP_EMU")) : 2;  // A/B knob (2: measured best)
+  auto go = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(bh * p.nqt), NUM_THREADS, SMEM_TOTAL, stream>>>(tK2, tV2, p);
+    return cudaGetLastError();
+  };
+  switch (emu_env) {
+    case 1: return go(simplicial_fwd_kernel<1>);
+    case 2: return go(simplicial_fwd_kernel<2>);
+    case 3: return go(simplicial_fwd_kernel<3>);
+    case 4: return go(simplicial_fwd_kernel<4>);
+    default: return go(simplicial_fwd_kernel<0>);
+  }
 }
 
 }  // namespace mimw

@@ -336,6 +336,42 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       return o;
     };
     bool o_live = false;  // O holds a folded U
+    bool fold_pending = false;  // U holds the complete U_d of the previous d
+    // ---- fold U_dd into O: O += v1[i - dd] (.) U_dd ----
+    auto fold = [&](int dd) {
+      TR(4, named_bar_sync(V1_FULL, V1_THREADS));
+#pragma unroll 1
+      for (int c = 64 * g; c < 64 * g + 64; c += 32) {
+        uint32_t u[32], o[32];
+        tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, u);
+        if (o_live) tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+          uint4 w;
+          const int ch = c / 8 + gg;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                       : "r"(sbase + SMEM_V1 + row * 256 + ((ch ^ (row & 15)) << 4)));
+          const uint32_t *pw = &w.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pw + e));
+            const int x = gg * 8 + e * 2;
+            const float b0 = o_live ? __uint_as_float(o[x]) : 0.f;
+            const float b1 = o_live ? __uint_as_float(o[x + 1]) : 0.f;
+            o[x] = __float_as_uint(b0 + f.x * __uint_as_float(u[x]));
+            o[x + 1] = __float_as_uint(b1 + f.y * __uint_as_float(u[x + 1]));
+          }
+        }
+        tmem_st_32x32b_x16(tmem + t_lane + TM_O + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
+        tmem_st_32x32b_x16(tmem + t_lane + TM_O + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
+      }
+      tmem_st_wait();
+      __syncwarp();
+      if (dd + 1 < nd) named_bar_arrive(V1_EMPTY, V1_THREADS);  // v1 rows of dd read
+      o_live = true;
+    };
     const float sl = p.scale_pos ? p.scale_log2 : 1.f;
     const uint64_t sl2 = f2_pack(sl, sl);
     for (int n = 0, d = 0, t = 0; n < nsteps; ++n, t = (t + 1 == ntile) ? 0 : t + 1, d += (t == 0)) {
@@ -363,10 +399,13 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
         uint64_t bits = 0;
         if (live && c_lo <= c_hi) bits = (~0ull >> (63 - c_hi)) & (~0ull << c_lo);
         const uint32_t b_lo = (uint32_t)bits, b_hi = (uint32_t)(bits >> 32);
+        if (!p.scale_pos) {  // uniform: scale not folded into the exponent FFMA
+#pragma unroll
+          for (int c = 0; c < 64; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
+        }
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           float v = __uint_as_float(s[c]);
-          if (!p.scale_pos) v *= p.scale_log2;
           const uint32_t w = c < 32 ? b_lo : b_hi;
           if (!(w & (1u << (c & 31)))) v = -INFINITY;
           s[c] = __float_as_uint(v);
@@ -409,12 +448,13 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       // P_n overwrites S buffer b, last read as P_{n-2} by PV(n-2)
       if (n >= 2) wait_pv(n - 2);
       if (__any_sync(0xffffffffu, rescale)) {
-        // U (this d's partial sum, if any PV of it ran) and O carry the old max
+        // U (this d's partial sum, or the previous d's complete U_{d-1} still
+        // waiting for its fold) and O carry the old max
         if (n >= 1) wait_pv(n - 1);
 #pragma unroll 1
         for (int c = 64 * g; c < 64 * g + 64; c += 32) {
           uint32_t o[32];
-          if (t > 0) {
+          if (t > 0 || fold_pending) {
             tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, o);
             tmem_ld_wait();
 #pragma unroll
@@ -434,49 +474,23 @@ simplicial_fwd_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_con
       }
       tmem_st_32x32b_x16(t_s, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       tmem_st_32x32b_x16(t_s + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+      if (fold_pending) {
+        // U_{d-1} is complete once PV(n-1) is; folded now, a step late, so
+        // the wait overlaps this step's softmax.  P_n is published after it:
+        // PV(n) (t == 0) overwrites U.
+        wait_pv(n - 1);
+        fold(d - 1);
+        fold_pending = false;
+      }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full(b));
-      if (t == ntile - 1) {
-        // ---- fold U_d into O: O += v1[i - d] (.) U_d (after this step's PV) ----
-        wait_pv(n);
-        TR(4, named_bar_sync(V1_FULL, V1_THREADS));
-#pragma unroll 1
-        for (int c = 64 * g; c < 64 * g + 64; c += 32) {
-          uint32_t u[32], o[32];
-          tmem_ld_32x32b_x32(tmem + t_lane + TM_U + c, u);
-          if (o_live) tmem_ld_32x32b_x32(tmem + t_lane + TM_O + c, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int gg = 0; gg < 4; ++gg) {
-            uint4 w;
-            const int ch = c / 8 + gg;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                         : "r"(sbase + SMEM_V1 + row * 256 + ((ch ^ (row & 15)) << 4)));
-            const uint32_t *pw = &w.x;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(pw + e));
-              const int x = gg * 8 + e * 2;
-              const float b0 = o_live ? __uint_as_float(o[x]) : 0.f;
-              const float b1 = o_live ? __uint_as_float(o[x + 1]) : 0.f;
-              o[x] = __float_as_uint(b0 + f.x * __uint_as_float(u[x]));
-              o[x + 1] = __float_as_uint(b1 + f.y * __uint_as_float(u[x + 1]));
-            }
-          }
-          tmem_st_32x32b_x16(tmem + t_lane + TM_O + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
-          tmem_st_32x32b_x16(tmem + t_lane + TM_O + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
-        }
-        tmem_st_wait();
-        __syncwarp();
-        if (d + 1 < nd) named_bar_arrive(V1_EMPTY, V1_THREADS);  // v1 rows of d read
-        o_live = true;
-        // the PV issuer overwrites U with the next d's first PV only after the
-        // next P arrives, which this warp publishes after these loads
-        tc_fence_before();
-      }
+      if (t == ntile - 1) fold_pending = true;
+    }
+    if (fold_pending) {
+      wait_pv(nsteps - 1);
+      fold(nd - 1);
     }
     // ---------------- epilogue: O / l, lse ----------------
     l += exchange(l);  // both groups' partial sums

@@ -81,8 +81,10 @@ template <int PAIRS>
 struct SchedT {
   static constexpr bool kGrouped = false;
   static constexpr bool kGather = false;
+  static constexpr bool kClc = true;
   static constexpr int kPairs = PAIRS;  // CTA pairs per cluster sharing each B tile (multicast)
   int num_m, num_n, group, M;           // num_m in cluster tiles (PAIRS M-tiles each)
+  int clc;                              // tiles dispatched by cluster launch control
   __device__ __forceinline__ int num_tiles() const { return num_m * num_n; }
   __device__ __forceinline__ TileCoord decode(int t) const {
     int per_group = group * num_n;
@@ -118,6 +120,7 @@ constexpr int MAX_GROUPS = 128;
 struct GroupedSched {
   static constexpr bool kGrouped = true;
   static constexpr bool kGather = false;
+  static constexpr bool kClc = true;
   static constexpr int kPairs = 1;
   CUtensorMap y[MAX_GROUPS];
   int order[MAX_GROUPS];           // slot -> group
@@ -192,7 +195,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   // 16-byte response + full barrier (completed by the response bytes) + empty
   // barrier on the pair leader (released by every consumer of both CTAs)
   constexpr int CLC_SLOTS = 4;
-  constexpr uint32_t CLC_CONSUMERS = CG * (1 + EPI_WARPS) + 1;  // producers, epilogue warps, MMA warp
+  // consumers: every CTA's producer and epilogue warps, and each pair leader's MMA warp
+  constexpr uint32_t CLC_CONSUMERS = CG * Prob::kPairs * (1 + EPI_WARPS) + Prob::kPairs;
   auto clc_resp = [&](int s) { return bar_base + 256 + 16 * s; };
   auto clc_full = [&](int s) { return bar_base + 256 + 16 * CLC_SLOTS + 8 * s; };
   auto clc_empty = [&](int s) { return bar_base + 256 + 24 * CLC_SLOTS + 8 * s; };
@@ -210,7 +214,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int num_tiles = sched.num_tiles();
   int num_k = (K + BK - 1) / BK;
   bool clc = false;
-  if constexpr (GROUPED) clc = sched.clc != 0;
+  if constexpr (Prob::kClc) clc = sched.clc != 0;
   bool comm = false;  // all-gather GEMM: the low cluster ids are comm pairs
   if constexpr (Prob::kGather) {
     static_assert(CG == 2 && B_MN && PAIRS == 1, "all-gather GEMM: 2-CTA, B as [K, N]");
@@ -257,16 +261,16 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     mbar_wait(clc_full(slot), (uint32_t)(u / CLC_SLOTS) & 1, 12);
     const int x = clc_query(clc_resp(slot));
     if (arrive) {
-      if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(clc_empty(slot), my_leader));
+      if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(clc_empty(slot), 0));  // on cluster rank 0
       else mbar_arrive(clc_empty(slot));
     }
     return x < 0 ? num_tiles : x / (CG * PAIRS);
   };
-  // Producer, at the start of tile u: the pair leader asks for tile u + 1
-  // (multicast to both CTAs); each CTA arms its own full barrier for it.
+  // Producer, at the start of tile u: cluster rank 0 asks for tile u + 1
+  // (multicast to every CTA of the cluster); each CTA arms its own full barrier.
   auto clc_request = [&](int u) {
     const int slot = u % CLC_SLOTS;
-    if (leader) {
+    if (crank == 0) {
       mbar_wait_cluster(clc_empty(slot), ((uint32_t)(u / CLC_SLOTS) & 1) ^ 1, 13);
       mbar_arrive_expect_tx(clc_full(slot), 16);
       if constexpr (CG == 2) clc_try_cancel_multicast(clc_resp(slot), clc_full(slot));
@@ -606,7 +610,7 @@ cudaError_t launch_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CU
   clusters -= comm_clusters;
   if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
   if (clusters > tiles) clusters = tiles;
-  if constexpr (Prob::kGrouped)
+  if constexpr (Prob::kClc)
     if (prob_in.clc) clusters = tiles;  // CLC: one cluster per tile, running clusters cancel the rest
   if (clusters <= 0 && tiles > 0) return cudaErrorInvalidConfiguration;
   if (clusters < 0) clusters = 0;
@@ -642,6 +646,8 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
   const int mt = (int)((g.m + BM_CTA * CG - 1) / (BM_CTA * CG));
   const int num_n = (int)((g.n + BN - 1) / BN);
   const int group = g.raster_group > 0 ? g.raster_group : 8;
+  static const int clc_env = getenv("MIMW_GEMM_CLC_DENSE") ? atoi(getenv("MIMW_GEMM_CLC_DENSE")) : 1;  // A/B knob (CLC measured +0.4%)
+  const int clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;
   if constexpr (CG == 2) {
     if (g.cluster_pairs == 2) {
       SchedT<2> s;
@@ -649,6 +655,7 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
       s.num_n = num_n;
       s.group = (group + 1) / 2;
       s.M = (int)g.m;
+      s.clc = clc;
       return launch_kernel<CG, B_MN, OutT>(tA, tB, tC, (int)g.n, (int)g.k, s, s.num_m * s.num_n,
                                            g.max_clusters, stream);
     }
@@ -658,6 +665,7 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
   s.num_n = num_n;
   s.group = group;
   s.M = (int)g.m;
+  s.clc = clc;
   return launch_kernel<CG, B_MN, OutT>(tA, tB, tC, (int)g.n, (int)g.k, s, s.num_m * s.num_n,
                                        g.max_clusters, stream);
 }

@@ -29,6 +29,7 @@ constexpr int COMM_W = 256;
 constexpr int COMM_MAX_BUFS = 24;
 struct GatherSched : SchedT<1> {
   static constexpr bool kGather = true;
+  static constexpr bool kClc = false;  // comm and GEMM CTAs must be co-resident: persistent grid
   CUtensorMap ga[MAX_SPLITS], gb[MAX_SPLITS];          // GEMM operands, rotation order (q = 0 local)
   CUtensorMap src_a[MAX_SPLITS], dst_a[MAX_SPLITS];    // comm: peer A rows -> landing (q >= 1)
   CUtensorMap src_b[MAX_SPLITS], dst_b[MAX_SPLITS];    // comm: peer B -> landing (q >= 1)

@@ -44,6 +44,14 @@ f = lambda: P.attention_bwd(q, k, v, o, do, lse, causal=False)
 flop = 2.5 * 4.0 * 128 * 4 * 48 * 8192 * 8192
 out = lambda: f()[0]
 ''',
+    "gemm": r'''
+a = (torch.rand((8192, 8192), device="cuda", generator=g) * 2 - 1).bfloat16()
+b = (torch.rand((8192, 8192), device="cuda", generator=g) * 2 - 1).bfloat16()
+c = torch.empty((8192, 8192), device="cuda", dtype=torch.bfloat16)
+f = lambda: P.gemm(a, b, out=c)
+flop = 2.0 * 8192 ** 3
+out = lambda: (f(), c)[1]
+''',
     "ln": r'''
 x = torch.randn((1152, 65536), device="cuda", generator=g)
 wt = torch.randn(65536, device="cuda", generator=g)

@@ -24,7 +24,8 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmimw_b200.so")
+# MIMW_B200_LIB: load another build of the library (A/B timing of two builds)
+LIB_PATH = os.environ.get("MIMW_B200_LIB") or os.path.join(PKG, "libmimw_b200.so")
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1

@@ -90,6 +90,17 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t lo, uint32_t hi) {
   return r;
 }
 
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -286,8 +297,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     const int ctid = (int)threadIdx.x - 128;  // 0..255 over the softmax warps
     if (n > 0 && ctid < 128) {
       const float *src = ctid < 64 ? p.lse2 : p.dvec;
-      *reinterpret_cast<float *>(smem + SM_LD + ctid * 4) =
-          __ldg(src + ((size_t)bh * p.nq + q_tile(0)) * BQ + (ctid & 63));
+      sts_f32(sbase + SM_LD + ctid * 4, __ldg(src + ((size_t)bh * p.nq + q_tile(0)) * BQ + (ctid & 63)));
     }
     named_bar_sync(1, 256);
     for (int t = 0; t < n; ++t) {
@@ -315,8 +325,10 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       uint32_t pk[16], dk2[16];
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 l4 = *reinterpret_cast<const float4 *>(smem + SM_LD + (t & 1) * 512 + (32 * ch + 4 * c4) * 4);
-        const float4 d4 = *reinterpret_cast<const float4 *>(smem + SM_LD + (t & 1) * 512 + 256 + (32 * ch + 4 * c4) * 4);
+        // explicit ld.shared (a generic pointer here compiled to LD.E: address
+        // translation and 2 wavefronts per broadcast load)
+        const float4 l4 = lds_f4(sbase + SM_LD + (t & 1) * 512 + (32 * ch + 4 * c4) * 4);
+        const float4 d4 = lds_f4(sbase + SM_LD + (t & 1) * 512 + 256 + (32 * ch + 4 * c4) * 4);
         const float la[4] = {l4.x, l4.y, l4.z, l4.w};
         const float da[4] = {d4.x, d4.y, d4.z, d4.w};
         float pv[4], dsv[4];
@@ -351,7 +363,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      if (ctid < 128) *reinterpret_cast<float *>(smem + SM_LD + ((t + 1) & 1) * 512 + ctid * 4) = pre;
+      if (ctid < 128) sts_f32(sbase + SM_LD + ((t + 1) & 1) * 512 + ctid * 4, pre);
       TR(3, named_bar_sync(1, 256));  // next step's lse2 / D visible; this step's reads done
     }
     // ---------------- epilogue: dV, dK (x scale) -> bf16 HBM ----------------

@@ -36,6 +36,8 @@
 #include "ptx.cuh"
 #include "tma_host.h"
 
+#include <type_traits>
+
 namespace mimw {
 
 namespace {
@@ -300,16 +302,16 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       sts_f32(sbase + SM_LD + ctid * 4, __ldg(src + ((size_t)bh * p.nq + q_tile(0)) * BQ + (ctid & 63)));
     }
     named_bar_sync(1, 256);
-    for (int t = 0; t < n; ++t) {
+    for (int t = 0, i = q_tile(0); t < n; ++t, i = (i == i_hi) ? i_lo : i + 1) {  // i = q_tile(t)
       const int s = t & 1;
-      const int i = q_tile(t);
+      const int i_next = (i == i_hi) ? i_lo : i + 1;
       // lse2 / D of the NEXT step: one value per thread (threads 0-63 lse2,
       // 64-127 D), loaded now, published into the smem double buffer at the end
       // of this step (named barrier among the softmax warps)
       float pre = 0.f;
       if (t + 1 < n && ctid < 128) {
         const float *src = ctid < 64 ? p.lse2 : p.dvec;
-        pre = __ldg(src + ((size_t)bh * p.nq + q_tile(t + 1)) * BQ + (ctid & 63));
+        pre = __ldg(src + ((size_t)bh * p.nq + i_next) * BQ + (ctid & 63));
       }
       TR(1, mbar_wait(s_full, t & 1, 7));
       tc_fence_after();
@@ -323,6 +325,10 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       if (lane == 0) mbar_arrive(dp_free);
       const int q0 = i * BQ + 32 * ch;
       uint32_t pk[16], dk2[16];
+      // per-score causal/window test only where some (key, query) pair of
+      // this CTA's 128 keys x this half's 32 queries is outside the band
+      const bool full = !p.causal || (j * BKV + BKV - 1 <= q0 && q0 + 31 - j * BKV < p.window);
+      auto scores = [&](auto masked) {
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         // explicit ld.shared (a generic pointer here compiled to LD.E: address
@@ -336,7 +342,7 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         for (int e = 0; e < 4; ++e) {
           const int c = 4 * c4 + e;
           const int qi = q0 + c;
-          const bool valid = !p.causal || (key <= qi && qi - key < p.window);
+          const bool valid = !decltype(masked)::value || (key <= qi && qi - key < p.window);
           const float x = __uint_as_float(sv[c]) * p.scale_log2 - la[e];
           const float pe = valid ? ex2(x) : 0.f;
           pv[e] = pe;
@@ -347,6 +353,9 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         dk2[2 * c4] = pack_bf16(dsv[0], dsv[1]);
         dk2[2 * c4 + 1] = pack_bf16(dsv[2], dsv[3]);
       }
+      };
+      if (full) scores(std::false_type{});
+      else scores(std::true_type{});
       // P^T | dS^T (bf16) over this half's S^T columns, already read
       tmem_st_32x32b_x16(t_s, pk);
       tmem_st_32x32b_x16(t_s + 16, dk2);

@@ -18,6 +18,7 @@
 #include "ptx.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mimw {
 
@@ -33,7 +34,7 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint
                : "memory");
 }
 
-// Block-wide sum; every thread gets the result.
+// Block-wide sum; every thread gets the result (xor butterfly over all 32 lanes).
 __device__ __forceinline__ float block_sum(float v, float *red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -43,7 +44,7 @@ __device__ __forceinline__ float block_sum(float v, float *red) {
   __syncthreads();
   float t = lane < THREADS / 32 ? red[lane] : 0.f;
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // every lane gets the total
   return t;
 }
 
@@ -169,6 +170,129 @@ layernorm_cluster_kernel(const float *__restrict__ x, const float *__restrict__ 
   cluster_sync();  // no CTA leaves while a peer's st.async may still target it
 }
 
+
+__device__ __forceinline__ void st_async_f32x2(uint32_t remote_addr, float a, float b, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                   remote_addr),
+               "f"(a), "f"(b), "r"(remote_bar)
+               : "memory");
+}
+
+// Look-ahead variant: ONE exchange per row (each CTA sends its slice's sum
+// and sum of squared deviations from the slice mean; Chan's pairwise
+// combination gives the row's mean and variance), sent one row AHEAD: row
+// k+1's partial statistics go out before row k is normalised, and row k's
+// were sent an iteration earlier, so a CTA only waits when a peer is a whole
+// row behind.  Rows k (normalising), k+1 (statistics) and k+2 (loads in
+// flight) are in registers.  Three exchange slots (row mod 3): a CTA sends
+// row k+1 only after receiving every peer's row k, by which time each peer
+// has consumed row k-2 from the slot being overwritten.  Needs vec_ok.
+template <int VPT>
+__global__ void __launch_bounds__(THREADS, 2)
+layernorm_cluster_la_kernel(const float *__restrict__ x, const float *__restrict__ w,
+                            const float *__restrict__ b, float *__restrict__ y, float *__restrict__ mean,
+                            float *__restrict__ rstd, int rows, int n, int slice, float eps) {
+  __shared__ float red[THREADS / 32];
+  __shared__ float2 xs[3][MAX_CLUSTER];
+  __shared__ alignas(8) uint64_t bars[3];
+  __shared__ float2 bc;
+  const uint32_t rank = cluster_ctarank();
+  const int nclusters = (int)nclusters_x();
+  const int csize = (int)(gridDim.x / nclusters);
+  const int c0 = (int)rank * slice;
+  const int c1 = min(n, c0 + slice);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    fence_mbar_init();
+  }
+  cluster_sync();
+
+  // local (sum, M2) of a slice in registers, sent to every peer's slot k % 3
+  auto send_stats = [&](const float4 (&v)[VPT], int k) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float ssum = block_sum(s, red);
+    const int nl = max(c1 - c0, 0);
+    const float lmu = nl > 0 ? ssum / (float)nl : 0.f;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = c0 + (i * THREADS + (int)threadIdx.x) * 4;
+      if (c < c1) {
+        const float dx = v[i].x - lmu, dy = v[i].y - lmu, dz = v[i].z - lmu, dw = v[i].w - lmu;
+        q += (dx * dx + dy * dy) + (dz * dz + dw * dw);
+      }
+    }
+    const float m2 = block_sum(q, red);
+    if (threadIdx.x == 0) {
+      const int slot = k % 3;
+      const uint32_t bar = smem_u32(&bars[slot]);
+      const uint32_t mine = smem_u32(&xs[slot][rank]);
+      xs[slot][rank] = make_float2(ssum, m2);
+      mbar_arrive_expect_tx(bar, 8u * (uint32_t)(csize - 1));
+      for (int p = 0; p < csize; ++p)
+        if (p != (int)rank) st_async_f32x2(map_to_rank(mine, (uint32_t)p), ssum, m2, map_to_rank(bar, (uint32_t)p));
+    }
+  };
+
+  const int row0 = (int)cluster_id_x();
+  float4 A[VPT], B[VPT], C[VPT];
+  if (row0 < rows) load_slice<VPT>(A, x + (size_t)row0 * n, c0, c1, 1);
+  if (row0 + nclusters < rows) load_slice<VPT>(B, x + (size_t)(row0 + nclusters) * n, c0, c1, 1);
+  if (row0 < rows) send_stats(A, 0);
+  int k = 0;
+  for (int row = row0; row < rows; row += nclusters, ++k) {
+    const int r1 = row + nclusters, r2 = row + 2 * nclusters;
+    if (r2 < rows) load_slice<VPT>(C, x + (size_t)r2 * n, c0, c1, 1);
+    if (threadIdx.x == 0) {
+      const int slot = k % 3;
+      mbar_wait(smem_u32(&bars[slot]), (uint32_t)(k / 3) & 1, 63);
+      float tot = 0.f;
+      for (int p = 0; p < csize; ++p) tot += xs[slot][p].x;
+      const float mu = tot / (float)n;
+      float m2 = 0.f;
+      for (int p = 0; p < csize; ++p) {
+        const int np = max(0, min(n, (p + 1) * slice) - p * slice);
+        if (np > 0) {
+          const float d = xs[slot][p].x / (float)np - mu;
+          m2 += xs[slot][p].y + (float)np * d * d;
+        }
+      }
+      const float rs = rsqrtf(m2 / (float)n + eps);
+      bc = make_float2(mu, rs);
+      if (rank == 0) {
+        if (mean) mean[row] = mu;
+        if (rstd) rstd[row] = rs;
+      }
+    }
+    __syncthreads();
+    const float2 st = bc;
+    if (r1 < rows) send_stats(B, k + 1);  // its block reductions also order every read of bc before the next write
+    float *yr = y + (size_t)row * n;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = c0 + (i * THREADS + (int)threadIdx.x) * 4;
+      if (c < c1) {
+        const float4 ww = __ldg(reinterpret_cast<const float4 *>(w + c));
+        const float4 bb = __ldg(reinterpret_cast<const float4 *>(b + c));
+        float4 o;
+        o.x = (A[i].x - st.x) * st.y * ww.x + bb.x;
+        o.y = (A[i].y - st.x) * st.y * ww.y + bb.y;
+        o.z = (A[i].z - st.x) * st.y * ww.z + bb.z;
+        o.w = (A[i].w - st.x) * st.y * ww.w + bb.w;
+        __stcs(reinterpret_cast<float4 *>(yr + c), o);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      A[i] = B[i];
+      B[i] = C[i];
+    }
+  }
+  cluster_sync();  // no CTA leaves while a peer's st.async may still target it
+}
+
 }  // namespace
 
 cudaError_t layernorm_cluster_launch(const LayerNormArgs &a, cudaStream_t stream) {
@@ -219,6 +343,30 @@ cudaError_t layernorm_cluster_launch(const LayerNormArgs &a, cudaStream_t stream
     return cudaLaunchKernelEx(&cfg, kern, a.x, a.w, a.b, a.y, a.mean, a.rstd, (int)a.rows, (int)a.n,
                               slice, (float)a.eps, vec_ok);
   };
+  auto go_la = [&](auto kern) -> cudaError_t {
+    if (csize > 8) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    int active = 0;
+    cfg.gridDim = dim3((unsigned)(std::min<int64_t>(a.rows, 4096) * csize), 1, 1);
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) != cudaSuccess || active <= 0) {
+      cudaGetLastError();
+      active = std::max(1, 148 / csize);
+    }
+    cfg.gridDim = dim3((unsigned)(std::min<int64_t>(a.rows, active) * csize), 1, 1);
+    return cudaLaunchKernelEx(&cfg, kern, a.x, a.w, a.b, a.y, a.mean, a.rstd, (int)a.rows, (int)a.n, slice,
+                              (float)a.eps);
+  };
+  static const int la_env = getenv("MIMW_LN_LOOKAHEAD") ? atoi(getenv("MIMW_LN_LOOKAHEAD")) : 1;  // A/B knob (1: measured +15%)
+  const bool vec_ok = (a.n % 4 == 0) &&
+                      ((((uintptr_t)a.x | (uintptr_t)a.w | (uintptr_t)a.b | (uintptr_t)a.y) & 15) == 0);
+  if (la_env && vec_ok) {
+    if (vec <= 1) return go_la(layernorm_cluster_la_kernel<1>);
+    if (vec <= 2) return go_la(layernorm_cluster_la_kernel<2>);
+    if (vec <= 4) return go_la(layernorm_cluster_la_kernel<4>);
+    if (vec <= 8) return go_la(layernorm_cluster_la_kernel<8>);
+  }
   if (vec <= 1) return go(layernorm_cluster_kernel<1>);
   if (vec <= 2) return go(layernorm_cluster_kernel<2>);
   if (vec <= 4) return go(layernorm_cluster_kernel<4>);

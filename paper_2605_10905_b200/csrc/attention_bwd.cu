@@ -34,6 +34,7 @@
 // (tcgen05.mma ops of one thread execute in issue order).
 #include "attention_bwd.h"
 #include "ptx.cuh"
+#include "pool.h"
 #include "tma_host.h"
 
 #include <type_traits>
@@ -521,21 +522,7 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
   // [bh, npad] f32
   const size_t acc_bytes = (size_t)bh * D * npad * 4;
   const size_t vec_bytes = (size_t)bh * npad * 4;
-  // stream-ordered scratch from the device's default pool, which is told to
-  // keep its memory (the default release threshold of 0 hands the ~0.8 GB
-  // accumulator back to the driver at every synchronisation and re-maps it on
-  // the next call: measured as tens of ms of jitter)
-  static bool pool_ready[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !pool_ready[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_ready[dev] = true;
-  }
+  keep_pool_memory();  // stream-ordered scratch, pool keeps its memory (pool.h)
   char *ws = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&ws), acc_bytes + 2 * vec_bytes + 256, stream);
   if (e != cudaSuccess) return e;

@@ -16,6 +16,7 @@
 
 #include "../../include/mimw_b200.h"
 #include "convert.h"
+#include "pool.h"
 #include "attention_fwd.h"
 #include "attention_bwd.h"
 #include "attention_f32.h"
@@ -109,6 +110,7 @@ struct DevBuf {
   void *p = nullptr;
   cudaStream_t s;
   DevBuf(size_t bytes, cudaStream_t st) : s(st) {
+    mimw::keep_pool_memory();
     if (bytes) check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
   }
   ~DevBuf() {

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <functional>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -17,6 +19,7 @@
 #include "../../include/mimw_b200.h"
 #include "convert.h"
 #include "pool.h"
+#include "host_stage.h"
 #include "attention_fwd.h"
 #include "attention_bwd.h"
 #include "attention_f32.h"
@@ -120,6 +123,102 @@ struct DevBuf {
   T *as() const { return static_cast<T *>(p); }
 };
 
+// MIMW_PREC_BF16 path of host_gemm with the f32 -> bf16 rounding done on the
+// host threads (host_stage.h) straight into the device layout in pinned
+// slots: PCIe carries 2 bytes per input element instead of 4, and the
+// conversion of chunk i+1 overlaps the DMA of chunk i.  Same bf16 values as
+// the device staging kernels, so the results are bit-identical.
+static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
+                                  const std::vector<const float *> &b_parts, const std::vector<int64_t> &k_parts,
+                                  int64_t m, int64_t n, int64_t k, float *c, cudaStream_t s, cudaStream_t cs,
+                                  cudaStream_t ds) {
+  const int64_t kp = round_up(k, 8);
+  const int64_t np = round_up(n, 8);
+  DevBuf dA(2 * m * kp, s), dB(2 * kp * np, s), dC(sizeof(float) * m * np, s);
+  Event e_alloc, e_b;
+  check_cuda(cudaEventRecord(e_alloc.e, s), "event");
+  check_cuda(cudaStreamWaitEvent(cs, e_alloc.e, 0), "wait");
+  check_cuda(cudaStreamWaitEvent(ds, e_alloc.e, 0), "wait");
+  std::vector<int64_t> koff(a_parts.size());
+  for (size_t i = 0, o = 0; i < a_parts.size(); o += k_parts[i], ++i) koff[i] = (int64_t)o;
+  std::vector<int> part_of_row((size_t)k);
+  for (size_t i = 0; i < a_parts.size(); ++i)
+    for (int64_t r = 0; r < k_parts[i]; ++r) part_of_row[(size_t)(koff[i] + r)] = (int)i;
+
+  const int64_t bchunk = std::max<int64_t>(64, round_up((k + 7) / 8, 8));
+  const int64_t achunk = std::max<int64_t>(512, round_up((m + 7) / 8, 256));
+  const size_t slot_bytes = (size_t)std::max(bchunk * np, achunk * kp) * 2;
+  constexpr int NSLOT = 3;
+  Event slot_ev[NSLOT];
+  bool slot_used[NSLOT] = {false, false, false};
+  int slot = 0;
+  // fill a pinned slot on the host threads, then DMA it to dst on cs
+  auto stage = [&](int64_t rows, const std::function<void(int64_t, uint16_t *)> &fill_row, int64_t pitch,
+                   void *dst) {
+    if (slot_used[slot]) check_cuda(cudaEventSynchronize(slot_ev[slot].e), "pinned slot reuse");
+    uint16_t *h = static_cast<uint16_t *>(mimw::pinned_slot(slot, slot_bytes));
+    require(h != nullptr, MIMW_ERR_CUDA, "cudaHostAlloc failed");
+    mimw::host_parallel_for(rows, [&](int64_t lo, int64_t hi) {
+      for (int64_t r = lo; r < hi; ++r) fill_row(r, h + r * pitch);
+    });
+    check_cuda(cudaMemcpyAsync(dst, h, (size_t)rows * pitch * 2, cudaMemcpyHostToDevice, cs), "H2D");
+    check_cuda(cudaEventRecord(slot_ev[slot].e, cs), "event");
+    slot_used[slot] = true;
+    slot = (slot + 1) % NSLOT;
+  };
+  // B rows (every part stacked along K), zero columns [n, np); zero rows [k, kp)
+  if (kp > k)
+    check_cuda(cudaMemsetAsync(static_cast<char *>(dB.p) + (size_t)k * np * 2, 0, (size_t)(kp - k) * np * 2, cs),
+               "memset");
+  for (int64_t r0 = 0; r0 < k; r0 += bchunk) {
+    const int64_t rows = std::min(bchunk, k - r0);
+    stage(rows, [&](int64_t r, uint16_t *dst) {
+      const int64_t kr = r0 + r;
+      const int i = part_of_row[(size_t)kr];
+      mimw::host_rows_to_bf16(b_parts[(size_t)i] + (kr - koff[(size_t)i]) * n, n, 1, n, dst, np, 0);
+      if (np > n) std::memset(dst + n, 0, (size_t)(np - n) * 2);
+    }, np, static_cast<char *>(dB.p) + (size_t)r0 * np * 2);
+  }
+  check_cuda(cudaEventRecord(e_b.e, cs), "event");
+  check_cuda(cudaStreamWaitEvent(s, e_b.e, 0), "wait");
+  const int nchunks = (int)((m + achunk - 1) / achunk);
+  std::vector<Event> e_a(nchunks), e_c(nchunks);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int64_t r0 = ci * achunk, rows = std::min(achunk, m - r0);
+    char *dA_rows = static_cast<char *>(dA.p) + (size_t)r0 * kp * 2;
+    stage(rows, [&](int64_t r, uint16_t *dst) {
+      for (size_t i = 0; i < a_parts.size(); ++i)
+        if (k_parts[i])
+          mimw::host_rows_to_bf16(a_parts[i] + (r0 + r) * k_parts[i], k_parts[i], 1, k_parts[i], dst, kp, koff[i]);
+      if (kp > k) std::memset(dst + k, 0, (size_t)(kp - k) * 2);
+    }, kp, dA_rows);
+    check_cuda(cudaEventRecord(e_a[ci].e, cs), "event");
+    check_cuda(cudaStreamWaitEvent(s, e_a[ci].e, 0), "wait");
+    mimw::GemmArgs g{};
+    g.a = dA_rows;
+    g.b = dB.p;
+    g.c = static_cast<char *>(dC.p) + (size_t)r0 * np * 4;
+    g.m = rows;
+    g.n = np;
+    g.k = kp;
+    g.lda = kp;
+    g.ldb = np;
+    g.ldc = np;
+    g.b_kn = true;
+    g.c_f32 = true;
+    g.cta_group = 2;
+    check_cuda(mimw::gemm_bf16_launch(g, s), "gemm launch");
+    check_cuda(cudaEventRecord(e_c[ci].e, s), "event");
+    check_cuda(cudaStreamWaitEvent(ds, e_c[ci].e, 0), "wait");
+    check_cuda(cudaMemcpy2DAsync(c + r0 * n, sizeof(float) * n, static_cast<char *>(dC.p) + (size_t)r0 * np * 4,
+                                 sizeof(float) * np, sizeof(float) * n, rows, cudaMemcpyDeviceToHost, ds),
+               "D2H c");
+  }
+  check_cuda(cudaStreamSynchronize(ds), "gemm execution");
+  check_cuda(cudaStreamSynchronize(cs), "gemm execution");
+  check_cuda(cudaStreamSynchronize(s), "gemm execution");
+}
+
 // C[m,n] (host f32) = sum_parts A_i[m,k_i] . B_i[k_i,n] on tensor cores.
 // The K-parts are concatenated along K (oracle_multi_device_gemm,
 // oracles.cpp:57-80); with MIMW_PREC_F32_BF16X3 every part is expanded to its
@@ -150,6 +249,11 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   cudaStream_t s = cudaStreamPerThread;
   cudaStream_t cs = side_stream(0), ds = side_stream(1);
   const int nseg = precision == MIMW_PREC_F32_BF16X3 ? 3 : 1;
+  static const int host_stage = getenv("MIMW_HOST_STAGE") ? atoi(getenv("MIMW_HOST_STAGE")) : 0;  // A/B knob (host rounding: 12.0 ms vs 11.4 ms device staging on 16 host cores)
+  if (nseg == 1 && host_stage) {
+    host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds);
+    return;
+  }
   const int64_t kp = round_up(k, 8);  // bf16 row pitch multiple of 16 B
   const int64_t np = round_up(n, 8);
   const int64_t kt = nseg * kp;

@@ -1,0 +1,150 @@
+// Host thread pool + pinned staging slots + f32 -> bf16 (RNE) row conversion
+// for the PCIe-bound host-Tile entries (host_stage.h).
+#include "host_stage.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace mimw {
+
+namespace {
+
+inline uint16_t bf16_rne(uint32_t u) {
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fff;  // NaN (the device conversion's canonical NaN)
+  return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+__attribute__((target("avx2"))) void convert_row_avx2(const float *src, int64_t n, uint16_t *dst) {
+  const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
+  for (int64_t j = 0; j < n; ++j) dst[j] = bf16_rne(s[j]);  // auto-vectorised with AVX2
+}
+
+void convert_row_generic(const float *src, int64_t n, uint16_t *dst) {
+  const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
+  for (int64_t j = 0; j < n; ++j) dst[j] = bf16_rne(s[j]);
+}
+
+class Pool {
+ public:
+  static Pool &get() {
+    static Pool p;
+    return p;
+  }
+  void run(int64_t n, const std::function<void(int64_t, int64_t)> &f) {
+    const int parts = (int)std::min<int64_t>(n, (int64_t)workers_.size() + 1);
+    if (parts <= 1) {
+      if (n > 0) f(0, n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(call_mu_);  // one parallel region at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      n_ = n;
+      parts_ = parts;
+      next_ = 1;
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0, n / parts);  // the caller takes part 0
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  Pool() {
+    unsigned hw = std::thread::hardware_concurrency();
+    int want = (int)std::min(hw ? hw : 4u, 16u);
+    if (const char *e = getenv("MIMW_HOST_THREADS")) want = std::max(1, atoi(e));  // A/B knob
+    const int nt = want - 1;
+    for (int i = 0; i < nt; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int64_t, int64_t)> *job;
+      int part;
+      int64_t n;
+      int parts;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || (gen_ != seen && job_ != nullptr && next_ < parts_); });
+        if (stop_) return;
+        part = next_++;
+        if (next_ >= parts_) seen = gen_;
+        job = job_;
+        n = n_;
+        parts = parts_;
+      }
+      (*job)(n * part / parts, n * (part + 1) / parts);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t, int64_t)> *job_ = nullptr;
+  int64_t n_ = 0;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace
+
+void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)> &f) { Pool::get().run(n, f); }
+
+void host_rows_to_bf16(const float *src, int64_t ld_src, int64_t rows, int64_t cols, uint16_t *dst,
+                       int64_t ld_dst, int64_t col_off) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  for (int64_t r = 0; r < rows; ++r) {
+    if (avx2) convert_row_avx2(src + r * ld_src, cols, dst + r * ld_dst + col_off);
+    else convert_row_generic(src + r * ld_src, cols, dst + r * ld_dst + col_off);
+  }
+}
+
+namespace {
+// per calling thread: concurrent host entries (the reference's oracles are
+// pure functions, safe to call from several threads) never share a buffer
+struct PinnedSlots {
+  std::vector<std::pair<void *, size_t>> v;
+  ~PinnedSlots() {
+    for (auto &s : v)
+      if (s.first) cudaFreeHost(s.first);
+  }
+};
+}  // namespace
+
+void *pinned_slot(int slot, size_t bytes) {
+  thread_local PinnedSlots slots;
+  if ((int)slots.v.size() <= slot) slots.v.resize((size_t)slot + 1, {nullptr, 0});
+  auto &s = slots.v[(size_t)slot];
+  if (s.second < bytes) {
+    if (s.first) cudaFreeHost(s.first);
+    s.first = nullptr;
+    s.second = 0;
+    if (cudaHostAlloc(&s.first, bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    s.second = bytes;
+  }
+  return s.first;
+}
+
+}  // namespace mimw

@@ -38,6 +38,8 @@
 #include "softmax.cuh"
 #include "tma_host.h"
 
+#include <cstdlib>
+
 namespace mimw {
 
 namespace {
@@ -77,6 +79,7 @@ struct Params {
   int scale_pos;     // scale > 0: max on raw scores, scale folded into FFMA2
   int *work_counter; // dynamic scheduler counter (zeroed before launch)
   unsigned long long *trace;  // optional per-warp cycle accounting [grid][12][8]
+  int dbg;           // timing-only probes (MIMW_FA_DEBUG): 1 = skip the O stores
 };
 
 // KV tile range [lo, hi] needed by Q rows [r0, r0 + 127]
@@ -193,6 +196,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
           // and can never run two phases ahead of this wait
           if (h == 1 && r0 + BQ >= p.seq) continue;
           mbar_wait(q_empty(h), qe_phase[h] ^ 1, 10);
+          EV(40 + h);
           mbar_arrive_expect_tx(q_full(h), TILE_BYTES);
           const uint32_t dq = sbase + SMEM_Q + h * TILE_BYTES;
           tma_load_3d(dq, &tmQ, q_full(h), 0, r0 + h * BQ, bh);
@@ -527,29 +531,40 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       mbar_wait(o_done(h), od_count & 1, 40 + h);
       ++od_count;
       tc_fence_after();
+      EV(30);
       const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
       if (row < p.seq) {
         if (p.lse != nullptr) p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(l)) * (1.0f / LOG2E);
       }
       uint4 *orow = reinterpret_cast<uint4 *>(p.o + ((size_t)bh * p.seq + row) * D);
+      const bool o_v8 = (reinterpret_cast<uintptr_t>(p.o) & 31) == 0;  // rows are 256 B: 32-B aligned base
 #pragma unroll 1
       for (int c = 0; c < 128; c += 32) {
         uint32_t o[32];
         tmem_ld_32x32b_x32(t_o + c, o);
         tmem_ld_wait();
-        if (row < p.seq) {
+        if (row < p.seq && p.dbg != 1) {
+          uint32_t w[16];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 w;
-            w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l);
-            w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l);
-            w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l);
-            w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l);
-            orow[c / 8 + v] = w;
+          for (int e = 0; e < 16; ++e)
+            w[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+          if (o_v8) {
+            // 256-bit stores (STG.E.ENL2.256): one full 32-B sector per lane,
+            // half the store instructions of the per-row epilogue
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c / 8 + 2 * v),
+                           "r"(w[8 * v]), "r"(w[8 * v + 1]), "r"(w[8 * v + 2]), "r"(w[8 * v + 3]),
+                           "r"(w[8 * v + 4]), "r"(w[8 * v + 5]), "r"(w[8 * v + 6]), "r"(w[8 * v + 7])
+                           : "memory");
+          } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) orow[c / 8 + v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
           }
         }
       }
       tc_fence_before();  // O_h read before the next item's first PV_h overwrites it
+      EV(31);
     }
 #ifdef MIMW_FA_TRACE
     if (p.trace && lane == 0)
@@ -595,6 +610,8 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   p.lse = a.lse;
   p.o = static_cast<__nv_bfloat16 *>(a.o);
   p.trace = a.trace;
+  static const int dbg = getenv("MIMW_FA_DEBUG") ? atoi(getenv("MIMW_FA_DEBUG")) : 0;
+  p.dbg = dbg;
   p.scale_pos = a.scale > 0 ? 1 : 0;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -131,10 +131,16 @@ struct DevBuf {
 static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
                                   const std::vector<const float *> &b_parts, const std::vector<int64_t> &k_parts,
                                   int64_t m, int64_t n, int64_t k, float *c, cudaStream_t s, cudaStream_t cs,
-                                  cudaStream_t ds) {
+                                  cudaStream_t ds, int mode) {
+  // mode 1: every chunk rounded on the host; 2: B's odd row chunks (and all of
+  // A) go over PCIe as f32 and are rounded by the device staging kernels, so
+  // the host threads and the H2D stream share B's transfer; 3: also A's odd
+  // chunks on the host
   const int64_t kp = round_up(k, 8);
   const int64_t np = round_up(n, 8);
   DevBuf dA(2 * m * kp, s), dB(2 * kp * np, s), dC(sizeof(float) * m * np, s);
+  DevBuf dF(mode == 1 ? 0 : sizeof(float) * (m + n) * k, s);  // f32 landing for device-rounded chunks
+  float *dFb = dF.as<float>(), *dFa = dF.as<float>() ? dF.as<float>() + (size_t)k * n : nullptr;
   Event e_alloc, e_b;
   check_cuda(cudaEventRecord(e_alloc.e, s), "event");
   check_cuda(cudaStreamWaitEvent(cs, e_alloc.e, 0), "wait");
@@ -170,8 +176,23 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
   if (kp > k)
     check_cuda(cudaMemsetAsync(static_cast<char *>(dB.p) + (size_t)k * np * 2, 0, (size_t)(kp - k) * np * 2, cs),
                "memset");
-  for (int64_t r0 = 0; r0 < k; r0 += bchunk) {
+  for (int64_t r0 = 0, bi = 0; r0 < k; r0 += bchunk, ++bi) {
     const int64_t rows = std::min(bchunk, k - r0);
+    if (mode != 1 && (bi & 1)) {
+      // f32 over PCIe, rounded by the device staging kernel (per K part)
+      for (size_t i = 0; i < b_parts.size(); ++i) {
+        const int64_t lo = std::max(r0, koff[i]), hi = std::min(r0 + rows, koff[i] + k_parts[i]);
+        if (hi <= lo) continue;
+        float *land = dFb + lo * n;
+        check_cuda(cudaMemcpyAsync(land, b_parts[i] + (lo - koff[i]) * n, sizeof(float) * (hi - lo) * n,
+                                   cudaMemcpyHostToDevice, cs), "H2D b");
+        Event e;
+        check_cuda(cudaEventRecord(e.e, cs), "event");
+        check_cuda(cudaStreamWaitEvent(s, e.e, 0), "wait");
+        mimw::stage_rows_bf16(land, hi - lo, hi - lo, n, np, dB.p, np, lo, 0, s);
+      }
+      continue;
+    }
     stage(rows, [&](int64_t r, uint16_t *dst) {
       const int64_t kr = r0 + r;
       const int i = part_of_row[(size_t)kr];
@@ -186,14 +207,33 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
   for (int ci = 0; ci < nchunks; ++ci) {
     const int64_t r0 = ci * achunk, rows = std::min(achunk, m - r0);
     char *dA_rows = static_cast<char *>(dA.p) + (size_t)r0 * kp * 2;
-    stage(rows, [&](int64_t r, uint16_t *dst) {
+    if (mode == 2 || (mode == 3 && (ci & 1))) {
+      // f32 over PCIe, rounded by the device staging kernel (per K part)
       for (size_t i = 0; i < a_parts.size(); ++i)
         if (k_parts[i])
-          mimw::host_rows_to_bf16(a_parts[i] + (r0 + r) * k_parts[i], k_parts[i], 1, k_parts[i], dst, kp, koff[i]);
-      if (kp > k) std::memset(dst + k, 0, (size_t)(kp - k) * 2);
-    }, kp, dA_rows);
-    check_cuda(cudaEventRecord(e_a[ci].e, cs), "event");
-    check_cuda(cudaStreamWaitEvent(s, e_a[ci].e, 0), "wait");
+          check_cuda(cudaMemcpyAsync(dFa + r0 * k + koff[i] * rows, a_parts[i] + r0 * k_parts[i],
+                                     sizeof(float) * rows * k_parts[i], cudaMemcpyHostToDevice, cs),
+                     "H2D a");
+      check_cuda(cudaEventRecord(e_a[ci].e, cs), "event");
+      check_cuda(cudaStreamWaitEvent(s, e_a[ci].e, 0), "wait");
+      for (size_t i = 0; i < a_parts.size(); ++i) {
+        const int64_t ki = k_parts[i];
+        if (ki == 0) continue;
+        const bool last = koff[i] + ki == k;
+        mimw::stage_cols_bf16(dFa + r0 * k + koff[i] * rows, rows, ki, last ? (kp - koff[i]) : ki, dA_rows, kp,
+                              koff[i], 0, s);
+      }
+    } else {
+      stage(rows, [&](int64_t r, uint16_t *dst) {
+        for (size_t i = 0; i < a_parts.size(); ++i)
+          if (k_parts[i])
+            mimw::host_rows_to_bf16(a_parts[i] + (r0 + r) * k_parts[i], k_parts[i], 1, k_parts[i], dst, kp,
+                                    koff[i]);
+        if (kp > k) std::memset(dst + k, 0, (size_t)(kp - k) * 2);
+      }, kp, dA_rows);
+      check_cuda(cudaEventRecord(e_a[ci].e, cs), "event");
+      check_cuda(cudaStreamWaitEvent(s, e_a[ci].e, 0), "wait");
+    }
     mimw::GemmArgs g{};
     g.a = dA_rows;
     g.b = dB.p;
@@ -251,7 +291,7 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   const int nseg = precision == MIMW_PREC_F32_BF16X3 ? 3 : 1;
   static const int host_stage = getenv("MIMW_HOST_STAGE") ? atoi(getenv("MIMW_HOST_STAGE")) : 0;  // A/B knob (host rounding: 12.0 ms vs 11.4 ms device staging on 16 host cores)
   if (nseg == 1 && host_stage) {
-    host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds);
+    host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds, host_stage);
     return;
   }
   const int64_t kp = round_up(k, 8);  // bf16 row pitch multiple of 16 B

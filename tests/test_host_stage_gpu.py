@@ -21,7 +21,7 @@ sys.path.insert(0, sys.argv[1])
 import paper_2605_10905_b200 as P
 out = {}
 rng = np.random.default_rng(7)
-for m, k, n in [(1, 1, 1), (37, 29, 45), (300, 200, 264), (1500, 136, 520)]:
+for m, k, n in [(1, 1, 1), (37, 29, 45), (300, 200, 264), (1500, 136, 520), (3000, 1100, 72)]:
     a = (rng.standard_normal((m, k)) * 3).astype(np.float32)
     b = (rng.standard_normal((k, n)) * 3).astype(np.float32)
     flat = a.reshape(-1)
@@ -48,8 +48,11 @@ def _run(tmp_path, flag):
     return np.load(path)
 
 
-def test_host_staging_bit_identical_to_device_staging(tmp_path):
-    host, dev = _run(tmp_path, 1), _run(tmp_path, 0)
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_host_staging_bit_identical_to_device_staging(tmp_path, mode):
+    """mode 1: all rounding on the host; 2: B's odd row chunks and all of A
+    rounded on the device; 3: odd chunks of both on the device."""
+    host, dev = _run(tmp_path, mode), _run(tmp_path, 0)
     assert sorted(host.files) == sorted(dev.files)
     for name in host.files:
         x, y = host[name], dev[name]

@@ -47,13 +47,14 @@ namespace {
 constexpr int D = 128;           // head dim (QK^T K-extent, PV N-extent)
 constexpr int BQ = 128;          // rows per Q tile (MMA M)
 constexpr int BKV = 128;         // keys per KV tile (S N-extent, PV K-extent)
-constexpr int NSLOT = 5;         // K/V ring slots (32 KiB each)
+constexpr int NSLOT = 4;         // K/V ring slots (32 KiB each; 5 measured the same)
 constexpr int TILE_BYTES = BKV * D * 2;  // 32 KiB: one Q, K or V tile
 constexpr int HALF_BYTES = TILE_BYTES / 2;  // one 64-column (128-B) swizzle panel
 constexpr int NUM_THREADS = 384;  // 3 warpgroups
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_KV = 2 * TILE_BYTES;
-constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
+constexpr int SMEM_O = SMEM_KV + NSLOT * TILE_BYTES;  // O staging: 8 softmax warps x 4 KiB (32 rows x 64 cols bf16)
+constexpr int SMEM_BAR = SMEM_O + 8 * 4096;
 constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);    // P (TMEM) x V (MN-major)
@@ -104,7 +105,7 @@ __device__ __forceinline__ void work_item(int idx, const Params &p, int &bh, int
 template <int EMU>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, Params p) {
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -536,36 +537,41 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       if (row < p.seq) {
         if (p.lse != nullptr) p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(l)) * (1.0f / LOG2E);
       }
-      uint4 *orow = reinterpret_cast<uint4 *>(p.o + ((size_t)bh * p.seq + row) * D);
-      const bool o_v8 = (reinterpret_cast<uintptr_t>(p.o) & 31) == 0;  // rows are 256 B: 32-B aligned base
+      // O / l through a per-warp 4 KiB smem box (32 rows x 64 columns, SW128)
+      // and a TMA store per half: coalesced, asynchronous, rows >= seq
+      // clipped by the tensor map (a thread per row storing straight to HBM
+      // touched 32 lines per warp store: ~3k cycles per item, measured)
+      const uint32_t obuf = sbase + SMEM_O + (uint32_t)(warp & 7) * 4096;
 #pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t o[32];
-        tmem_ld_32x32b_x32(t_o + c, o);
-        tmem_ld_wait();
-        if (row < p.seq && p.dbg != 1) {
-          uint32_t w[16];
+      for (int half = 0; half < 2; ++half) {
+        uint32_t w[32];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(t_o + 64 * half + 32 * cc, o);
+          tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            w[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-          if (o_v8) {
-            // 256-bit stores (STG.E.ENL2.256): one full 32-B sector per lane,
-            // half the store instructions of the per-row epilogue
+            w[16 * cc + e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+        }
+        if (lane == 0) bulk_wait_read<0>();  // the previous store from this box has read it
+        __syncwarp();
 #pragma unroll
-            for (int v = 0; v < 2; ++v)
-              asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c / 8 + 2 * v),
-                           "r"(w[8 * v]), "r"(w[8 * v + 1]), "r"(w[8 * v + 2]), "r"(w[8 * v + 3]),
-                           "r"(w[8 * v + 4]), "r"(w[8 * v + 5]), "r"(w[8 * v + 6]), "r"(w[8 * v + 7])
-                           : "memory");
-          } else {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) orow[c / 8 + v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
-          }
+        for (int c = 0; c < 8; ++c)
+          st_shared_v4(obuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2],
+                       w[4 * c + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0 && p.dbg != 1) {
+          tma_store_3d(&tmO, obuf, 64 * half, rt + q * 32, bh);
+          bulk_commit();
         }
       }
       tc_fence_before();  // O_h read before the next item's first PV_h overwrites it
       EV(31);
     }
+    if (lane == 0) bulk_wait<0>();  // this warp's O stores done before its smem box goes away
+    __syncwarp();
 #ifdef MIMW_FA_TRACE
     if (p.trace && lane == 0)
       for (int e = 0; e < 8; ++e) p.trace[((size_t)blockIdx.x * 12 + warp) * 8 + e] = tr_acc[e];
@@ -598,6 +604,8 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
                                 (uint64_t)a.seq * D, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tK = make_tmap_3d(a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tO = make_tmap_3d(a.o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                (uint64_t)a.seq * D, 64, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tV = make_tmap_3d(a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   Params p;
@@ -626,7 +634,7 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   auto launch = [&](auto kern) {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e2 != cudaSuccess) return e2;
-    kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, p);
+    kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, tO, p);
     return cudaGetLastError();
   };
   switch (a.emu < 0 ? kDefaultEmu : a.emu) {

@@ -589,7 +589,8 @@ def bench_layernorm(args, rank, ws, local):
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm"],
                          "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
                          "peak_source": f"{pk['src']} HBM copy bandwidth",
-                         "algorithmic_bytes_per_launch": 8.0 * rows * n, "traffic": None},
+                         "algorithmic_bytes_per_launch": 8.0 * rows * n,
+                         "traffic": traffic("layernorm_ln6") if ws == 1 else None},
             "clocks": clocks}
 
 

@@ -3,7 +3,7 @@
 #   launches.csv         every launch of a short default bench with its device time
 #                        (cold-cache, serialised: compare SHARES, not absolutes)
 #   <name>.ncu-rep       one `--set full` capture of each top kernel
-# Usage: tools/profile.sh [launches] [gemm] [fa] [fp8] [moe]
+# Usage: tools/profile.sh [launches] [gemm] [fa] [fp8] [moe] [ln] [md] [bwd] [simp]
 set -u
 OUT=${OUT:-gpurun_out}
 mkdir -p "$OUT"
@@ -31,6 +31,10 @@ for what in "$@"; do
       timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
         -k regex:GroupedSched -s 3 -c 1 -o "$OUT/moe" -f \
         python bench.py --workload moe --steps 1 --warmup 3 --no-cpu > "$OUT/moe_ncu.log" 2>&1 ;;
+    ln)
+      timeout 900 $NCU --set full --import-source on -k regex:layernorm_cluster -s 3 -c 1 \
+        -o "$OUT/ln" -f python bench.py --workload layernorm --steps 2 --warmup 3 --no-cpu \
+        > "$OUT/ln_ncu.log" 2>&1 ;;
     md)
       timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
         -k regex:GatherSched -s 3 -c 1 -o "$OUT/md" -f \

@@ -547,7 +547,7 @@ cudaError_t simplicial_fwd_launch(const SimplicialArgs &a, cudaStream_t stream) 
   p.nqt = (int)((a.seq + BQ - 1) / BQ);
   p.scale_log2 = (float)(a.scale * 1.4426950408889634);
   p.scale_pos = a.scale > 0 ? 1 : 0;
-  static const int emu_env = getenv("MIMW_SIMP_EMU") ? atoi(getenv("MIMW_SIMP_EMU")) : 2;  // A/B knob (2: measured best)
+  static const int emu_env = getenv("MIMW_SIMP_EMU") ? atoi(getenv("MIMW_SIMP_EMU")) : 1;  // A/B knob (1: 661, 2: 659, 3: 648 TF measured)
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;

@@ -37,6 +37,12 @@ f = lambda: P.attention_fwd(q, k, v)
 flop = 4.0 * 128 * 4 * 32 * 8192 * 8193 / 2
 out = lambda: f()[0]
 ''',
+    "fa_emu": r'''
+q, k, v = ((torch.rand((4, 32, 8192, 128), device="cuda", generator=g) * 2 - 1).bfloat16() for _ in range(3))
+f = lambda: P.attention_fwd(q, k, v, emu=int(os.environ.get("AB_EMU", "-1")))
+flop = 4.0 * 128 * 4 * 32 * 8192 * 8193 / 2
+out = lambda: f()[0]
+''',
     "fa1k": r'''
 q, k, v = ((torch.rand((1, 8192, 1024, 128), device="cuda", generator=g) * 2 - 1).bfloat16() for _ in range(3))
 f = lambda: P.attention_fwd(q, k, v)

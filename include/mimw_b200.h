@@ -64,7 +64,8 @@ int mimw_b200_oracle_gemm(const float *a, const float *b, float *c, int64_t m, i
 /* Device form: a bf16 [m, lda], b bf16 ([k, ldb] for MIMW_B_KN or [n, ldb]
  * for MIMW_B_NK), c [m, ldc] of c_dtype (MIMW_F32 or MIMW_BF16).  Leading
  * dimensions in elements; row pitches must be multiples of 16 bytes (TMA).
- * Persistent warp-specialized kernel, 2-CTA clusters (cta_group::2). */
+ * Warp-specialized kernel, 2-CTA clusters (cta_group::2); output tiles are
+ * dispatched by hardware cluster launch control (gemm_clc.mimw). */
 int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_t n, int64_t k,
                         int64_t lda, int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype,
                         void *stream);
@@ -87,8 +88,9 @@ int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const vo
  * y bf16 [m_offsets[G], n] are DEVICE buffers with rows packed by group;
  * m_offsets is a HOST int64 array of n_groups + 1 non-decreasing row offsets
  * (empty groups allowed); w bf16 is [G, k, n] (MIMW_B_KN, the reference's
- * B layout) or [G, n, k] (MIMW_B_NK).  n and k multiples of 8.  Persistent
- * 2-CTA kernel; each group's tail tile is clipped by its own Y tensor map. */
+ * B layout) or [G, n, k] (MIMW_B_NK).  n and k multiples of 8.  2-CTA kernel,
+ * tiles dispatched by cluster launch control; each group's < 256-row tail runs
+ * as a swapped-operand tile clipped by the group's own Y tensor map. */
 int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const void *w, void *y,
                                 int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
                                 void *stream);

@@ -321,7 +321,7 @@ def bench_gemm(args, rank, ws, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic U[-1,1] bf16 (random init, no dataset)",
-        "config": {"workload": "configs[1]: persistent warp-specialized bf16 GEMM M=N=K=8192, "
+        "config": {"workload": "configs[1]: warp-specialized bf16 GEMM M=N=K=8192 (tiles by cluster launch control), "
                                "2-CTA clusters (cta_group::2), fp32 accumulate in TMEM, bf16 out",
                    "M": GEMM_M, "N": GEMM_N, "K": GEMM_K, "tile": "256x256x64, 6-stage ring",
                    "parallelism": f"{ws} independent GEMM batches (one per GPU)",

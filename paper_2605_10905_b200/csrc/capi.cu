@@ -289,7 +289,7 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   cudaStream_t s = cudaStreamPerThread;
   cudaStream_t cs = side_stream(0), ds = side_stream(1);
   const int nseg = precision == MIMW_PREC_F32_BF16X3 ? 3 : 1;
-  static const int host_stage = getenv("MIMW_HOST_STAGE") ? atoi(getenv("MIMW_HOST_STAGE")) : 0;  // A/B knob (host rounding: 12.0 ms vs 11.4 ms device staging on 16 host cores)
+  static const int host_stage = getenv("MIMW_HOST_STAGE") ? atoi(getenv("MIMW_HOST_STAGE")) : 3;  // A/B knob (mode 3 9.9-10.0 ms vs device staging 11.2)
   if (nseg == 1 && host_stage) {
     host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds, host_stage);
     return;

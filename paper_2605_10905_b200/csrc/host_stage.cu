@@ -3,6 +3,7 @@
 #include "host_stage.h"
 
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -21,9 +22,32 @@ inline uint16_t bf16_rne(uint32_t u) {
   return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
 }
 
+__attribute__((target("avx2"))) inline __m256i cvt8_avx2(__m256i u) {
+  const __m256i is_nan = _mm256_cmpgt_epi32(_mm256_and_si256(u, _mm256_set1_epi32(0x7fffffff)),
+                                            _mm256_set1_epi32(0x7f800000));
+  const __m256i lsb = _mm256_and_si256(_mm256_srli_epi32(u, 16), _mm256_set1_epi32(1));
+  const __m256i r = _mm256_srli_epi32(_mm256_add_epi32(_mm256_add_epi32(u, _mm256_set1_epi32(0x7fff)), lsb), 16);
+  return _mm256_blendv_epi8(r, _mm256_set1_epi32(0x7fff), is_nan);
+}
+
+// 16 elements per iteration, streaming (non-temporal) 32-B stores into the
+// pinned slot: no read-for-ownership of the destination lines, which the DMA
+// engine reads next anyway
 __attribute__((target("avx2"))) void convert_row_avx2(const float *src, int64_t n, uint16_t *dst) {
   const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
-  for (int64_t j = 0; j < n; ++j) dst[j] = bf16_rne(s[j]);  // auto-vectorised with AVX2
+  int64_t j = 0;
+  while (j < n && (reinterpret_cast<uintptr_t>(dst + j) & 31)) {
+    dst[j] = bf16_rne(s[j]);
+    ++j;
+  }
+  for (; j + 16 <= n; j += 16) {
+    const __m256i a = cvt8_avx2(_mm256_loadu_si256(reinterpret_cast<const __m256i *>(s + j)));
+    const __m256i b = cvt8_avx2(_mm256_loadu_si256(reinterpret_cast<const __m256i *>(s + j + 8)));
+    // packus works per 128-bit lane: a0-3 b0-3 | a4-7 b4-7 -> reorder the 64-bit quarters
+    const __m256i p = _mm256_permute4x64_epi64(_mm256_packus_epi32(a, b), 0xD8);
+    _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + j), p);
+  }
+  for (; j < n; ++j) dst[j] = bf16_rne(s[j]);
 }
 
 void convert_row_generic(const float *src, int64_t n, uint16_t *dst) {
@@ -119,6 +143,7 @@ void host_rows_to_bf16(const float *src, int64_t ld_src, int64_t rows, int64_t c
     if (avx2) convert_row_avx2(src + r * ld_src, cols, dst + r * ld_dst + col_off);
     else convert_row_generic(src + r * ld_src, cols, dst + r * ld_dst + col_off);
   }
+  if (avx2) _mm_sfence();  // streaming stores ordered before the caller hands the slot to the DMA
 }
 
 namespace {

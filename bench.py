@@ -154,6 +154,29 @@ def max_over_ranks(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def e2e_h2d_bytes(m, n, k):
+    """H2D bytes of one mimw_b200_oracle_gemm call (PREC_BF16), following the
+    chunking of capi.cu host_gemm_host_staged: row chunks of B (k/8 rows) and A
+    (m/8 rows); MIMW_HOST_STAGE 0 = all f32, 1 = all bf16, 2 = B's odd chunks
+    and all of A f32, 3 (default) = odd chunks of both f32, the rest bf16."""
+    mode = int(os.environ.get("MIMW_HOST_STAGE", "3"))
+    r8 = lambda x, q: (x + q - 1) // q * q  # noqa: E731
+    kp, np_ = r8(k, 8), r8(n, 8)
+    if mode == 0:
+        return 4 * (m * k + k * n)
+    bchunk = max(64, r8((k + 7) // 8, 8))
+    achunk = max(512, r8((m + 7) // 8, 256))
+    total = 0
+    for i, r0 in enumerate(range(0, k, bchunk)):
+        rows = min(bchunk, k - r0)
+        total += 4 * rows * n if (mode != 1 and i % 2 == 1) else 2 * rows * np_
+    for i, r0 in enumerate(range(0, m, achunk)):
+        rows = min(achunk, m - r0)
+        f32 = mode == 2 or (mode == 3 and i % 2 == 1)
+        total += 4 * rows * k if f32 else 2 * rows * kp
+    return total
+
+
 def timed(step, steps, warmup, ws, stream):
     """W warm-up steps, then K steps between barrier+synchronize, CUDA events
     on the launching stream; returns max-over-ranks seconds for the K steps."""
@@ -309,7 +332,7 @@ def bench_gemm(args, rank, ws, local):
             e2e_step()
         dt = max_over_ranks((time.perf_counter() - t0) / n_e2e, ws)
         e2e = {"value": round(ws * flop / dt / 1e12, 2), "unit": "TFLOPS",
-               "h2d_bytes_per_step": 4 * (GEMM_M * GEMM_K + GEMM_K * GEMM_N),
+               "h2d_bytes_per_step": e2e_h2d_bytes(GEMM_M, GEMM_N, GEMM_K),
                "d2h_bytes_per_step": 4 * GEMM_M * GEMM_N,
                "api": "mimw_b200_oracle_gemm (host f32 Tiles, include/mimw_b200.h)",
                "ms_per_step": round(dt * 1e3, 3)}

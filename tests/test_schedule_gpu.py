@@ -1,9 +1,10 @@
 """Schedule independence: the B200 analogue of the reference's 100-seed
 schedule-robustness criterion (acceptance.cpp:428-486, test_kernels.cpp:37-61)
-and of CLC exactly-once (test_clc.cpp:25-92).  The persistent kernels hand out
-work through different paths depending on how many CTAs run: static striding
-(GEMM, grouped GEMM) or the atomic work counter published through a 2-slot
-mbarrier ring with a -1 sentinel (attention forward).  Every tile must be
+and of CLC exactly-once (test_clc.cpp:25-92).  The kernels hand out work
+through different paths: hardware cluster launch control (GEMM and grouped
+GEMM by default, max_clusters=0), persistent static striding (max_clusters > 0)
+or the atomic work counter published through a 2-slot mbarrier ring with a -1
+sentinel (attention forward).  Every tile must be
 computed exactly once, in the same arithmetic order, whatever the CTA count,
 so the results must be bit-identical across grid sizes."""
 import numpy as np

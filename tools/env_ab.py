@@ -60,7 +60,8 @@ out = lambda: f()[0]
 a = (torch.rand((8192, 8192), device="cuda", generator=g) * 2 - 1).bfloat16()
 b = (torch.rand((8192, 8192), device="cuda", generator=g) * 2 - 1).bfloat16()
 c = torch.empty((8192, 8192), device="cuda", dtype=torch.bfloat16)
-f = lambda: P.gemm(a, b, out=c)
+f = lambda: P.gemm(a, b, out=c, cta_group=int(os.environ.get("AB_CG", "2")),
+                   raster_group=int(os.environ.get("AB_RASTER", "0")))
 flop = 2.0 * 8192 ** 3
 out = lambda: (f(), c)[1]
 ''',

@@ -54,18 +54,20 @@ __device__ __forceinline__ float block_sum(float v, float *red) {
 __device__ __forceinline__ float cluster_sum(float part, int round, int csize, uint32_t rank,
                                              float *slots, uint32_t bar, uint32_t parity,
                                              float *bcast) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: lane p sends to peer p, then the lanes sum the slots
+    const int p = (int)threadIdx.x;
     const uint32_t my_slot = smem_u32(slots + round * MAX_CLUSTER + rank);
-    slots[round * MAX_CLUSTER + rank] = part;
-    mbar_arrive_expect_tx(bar, 4u * (uint32_t)(csize - 1));
-    for (int p = 0; p < csize; ++p) {
-      if (p == (int)rank) continue;
-      st_async_f32(map_to_rank(my_slot, (uint32_t)p), part, map_to_rank(bar, (uint32_t)p));
+    if (p == 0) {
+      slots[round * MAX_CLUSTER + rank] = part;
+      mbar_arrive_expect_tx(bar, 4u * (uint32_t)(csize - 1));
     }
+    if (p < csize && p != (int)rank) st_async_f32(map_to_rank(my_slot, (uint32_t)p), part, map_to_rank(bar, (uint32_t)p));
     mbar_wait(bar, parity, 60 + round);
-    float s = 0.f;
-    for (int p = 0; p < csize; ++p) s += slots[round * MAX_CLUSTER + p];
-    *bcast = s;
+    __syncwarp();  // lane 0's own-slot write visible to lane `rank`
+    float s = p < csize ? slots[round * MAX_CLUSTER + p] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (p == 0) *bcast = s;
   }
   __syncthreads();
   return *bcast;
@@ -225,14 +227,17 @@ layernorm_cluster_la_kernel(const float *__restrict__ x, const float *__restrict
       }
     }
     const float m2 = block_sum(q, red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: lane p sends to peer p
       const int slot = k % 3;
       const uint32_t bar = smem_u32(&bars[slot]);
       const uint32_t mine = smem_u32(&xs[slot][rank]);
-      xs[slot][rank] = make_float2(ssum, m2);
-      mbar_arrive_expect_tx(bar, 8u * (uint32_t)(csize - 1));
-      for (int p = 0; p < csize; ++p)
-        if (p != (int)rank) st_async_f32x2(map_to_rank(mine, (uint32_t)p), ssum, m2, map_to_rank(bar, (uint32_t)p));
+      if (threadIdx.x == 0) {
+        xs[slot][rank] = make_float2(ssum, m2);
+        mbar_arrive_expect_tx(bar, 8u * (uint32_t)(csize - 1));
+      }
+      const int p = (int)threadIdx.x;
+      if (p < csize && p != (int)rank)
+        st_async_f32x2(map_to_rank(mine, (uint32_t)p), ssum, m2, map_to_rank(bar, (uint32_t)p));
     }
   };
 
@@ -245,25 +250,27 @@ layernorm_cluster_la_kernel(const float *__restrict__ x, const float *__restrict
   for (int row = row0; row < rows; row += nclusters, ++k) {
     const int r1 = row + nclusters, r2 = row + 2 * nclusters;
     if (r2 < rows) load_slice<VPT>(C, x + (size_t)r2 * n, c0, c1, 1);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0 combines: lane p holds peer p's (sum, M2)
       const int slot = k % 3;
+      const int p = (int)threadIdx.x;
       mbar_wait(smem_u32(&bars[slot]), (uint32_t)(k / 3) & 1, 63);
-      float tot = 0.f;
-      for (int p = 0; p < csize; ++p) tot += xs[slot][p].x;
+      const float2 sp = p < csize ? xs[slot][p] : make_float2(0.f, 0.f);
+      float tot = sp.x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       const float mu = tot / (float)n;
-      float m2 = 0.f;
-      for (int p = 0; p < csize; ++p) {
-        const int np = max(0, min(n, (p + 1) * slice) - p * slice);
-        if (np > 0) {
-          const float d = xs[slot][p].x / (float)np - mu;
-          m2 += xs[slot][p].y + (float)np * d * d;
+      const int np = p < csize ? max(0, min(n, (p + 1) * slice) - p * slice) : 0;
+      const float d = np > 0 ? sp.x / (float)np - mu : 0.f;
+      float m2 = np > 0 ? sp.y + (float)np * d * d : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+      if (p == 0) {
+        const float rs = rsqrtf(m2 / (float)n + eps);
+        bc = make_float2(mu, rs);
+        if (rank == 0) {
+          if (mean) mean[row] = mu;
+          if (rstd) rstd[row] = rs;
         }
-      }
-      const float rs = rsqrtf(m2 / (float)n + eps);
-      bc = make_float2(mu, rs);
-      if (rank == 0) {
-        if (mean) mean[row] = mu;
-        if (rstd) rstd[row] = rs;
       }
     }
     __syncthreads();

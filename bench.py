@@ -107,7 +107,15 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows if len(r) >= 8
                           for i in range(4) if r[4 + i].lower().startswith("active")})
-        loaded = [s for s in sm if s > 500] or sm
+        # "under load": samples drawing > 40% of the peak power seen (the 50-ms
+        # sampler also catches the idle edges around a short timed region)
+        pw = [float(r[2]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()
+              and r[2].replace(".", "").isdigit()]
+        if len(pw) == len(sm) and pw:
+            loaded = [s_ for s_, w_ in zip(sm, pw) if w_ > 0.4 * max(pw)]
+        else:
+            loaded = [s_ for s_ in sm if s_ > 500]
+        loaded = loaded or sm
         return {"sm_mhz": float(np.median(loaded)) if loaded else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(sm)}

@@ -36,6 +36,7 @@
 #include "attention_fwd.h"
 #include "ptx.cuh"
 #include "softmax.cuh"
+#include "pool.h"
 #include "tma_host.h"
 
 #include <cstdlib>
@@ -588,16 +589,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 
 }  // namespace
 
-// per-device scheduler counters (zeroed on the launch stream before every launch)
-static int *work_counter(int device) {
-  static int *ctr[64] = {nullptr};
-  if (device < 0 || device >= 64) return nullptr;
-  if (!ctr[device]) {
-    if (cudaMalloc(&ctr[device], sizeof(int)) != cudaSuccess) return nullptr;
-  }
-  return ctr[device];
-}
-
 cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   const uint64_t bh = (uint64_t)a.batch * a.heads;
   CUtensorMap tQ = make_tmap_3d(a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
@@ -621,29 +612,33 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   static const int dbg = getenv("MIMW_FA_DEBUG") ? atoi(getenv("MIMW_FA_DEBUG")) : 0;
   p.dbg = dbg;
   p.scale_pos = a.scale > 0 ? 1 : 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  p.work_counter = work_counter(dev);
-  if (!p.work_counter) return cudaErrorMemoryAllocation;
   const int items = p.bh * p.nqb;
   int grid = sm_count();
   if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
   if (grid > items) grid = items;
-  cudaError_t e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
+  // The scheduler counter is per launch, stream-ordered scratch: launches on
+  // different streams (or host threads) never share it.
+  keep_pool_memory();
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p.work_counter), sizeof(int), stream);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
   auto launch = [&](auto kern) {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e2 != cudaSuccess) return e2;
     kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, tO, p);
     return cudaGetLastError();
   };
-  switch (a.emu < 0 ? kDefaultEmu : a.emu) {
-    case 0: return launch(attention_fwd_kernel<0>);
-    case 1: return launch(attention_fwd_kernel<1>);
-    case 2: return launch(attention_fwd_kernel<2>);
-    case 3: return launch(attention_fwd_kernel<3>);
-    default: return launch(attention_fwd_kernel<4>);
+  if (e == cudaSuccess) {
+    switch (a.emu < 0 ? kDefaultEmu : a.emu) {
+      case 0: e = launch(attention_fwd_kernel<0>); break;
+      case 1: e = launch(attention_fwd_kernel<1>); break;
+      case 2: e = launch(attention_fwd_kernel<2>); break;
+      case 3: e = launch(attention_fwd_kernel<3>); break;
+      default: e = launch(attention_fwd_kernel<4>); break;
+    }
   }
+  const cudaError_t e3 = cudaFreeAsync(p.work_counter, stream);
+  return e != cudaSuccess ? e : e3;
 }
 
 }  // namespace mimw

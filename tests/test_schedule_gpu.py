@@ -74,3 +74,26 @@ def test_multi_device_gemm_bitwise_across_comm_modes(P):
         for conc in (False, True):
             out = MD.emulated_multi_device_gemm(a, b, comm_pairs=cp, concurrent=conc)
             assert torch.equal(out, ref), (cp, conc)
+
+
+def test_attention_concurrent_streams_bitwise(P):
+    """Two forward launches in flight on different streams (the host entries
+    run one stream per calling thread): each launch's work counter is its own
+    stream-ordered scratch, so both outputs equal their one-at-a-time runs."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(9)
+    qs = [[(torch.rand((1, 8, 2048, 128), device="cuda", generator=g) * 2 - 1).bfloat16() for _ in range(3)]
+          for _ in range(2)]
+    ref = [P.attention_fwd(*t)[0].clone() for t in qs]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            o1 = P.attention_fwd(*qs[0])[0]  # current stream = s1
+        with torch.cuda.stream(s2):
+            o2 = P.attention_fwd(*qs[1])[0]  # current stream = s2
+        outs.append((o1, o2))
+    torch.cuda.synchronize()
+    for o1, o2 in outs:
+        assert torch.equal(o1, ref[0]) and torch.equal(o2, ref[1])

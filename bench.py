@@ -124,26 +124,53 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
+def backend_for(ws: int) -> str:
+    """nccl (one rank per GPU), or gloo when MIMW_BENCH_BACKEND says so or the
+    box has fewer GPUs than ranks (ranks then share GPUs: a functional check
+    of the multi-rank path, not a scaling measurement)."""
+    import torch
+    b = os.environ.get("MIMW_BENCH_BACKEND")
+    if b:
+        return b
+    return "nccl" if torch.cuda.device_count() >= ws else "gloo"
+
+
 def dist_init(n_gpus):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={ws} ranks were launched")
     if ws > 1:
         import torch.distributed as dist
-        # MIMW_BENCH_BACKEND=gloo runs every rank on the visible GPU(s) modulo
-        # their count: a functional check of the multi-rank paths on a 1-GPU box
-        # (numbers from such a run are not scaling measurements)
-        backend = os.environ.get("MIMW_BENCH_BACKEND", "nccl")
-        local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
+        backend = backend_for(ws) if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        assert dist.get_world_size() == n_gpus
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, ws, local
+
+
+def relaunch(n_gpus: int) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-exec under
+    torchrun with one rank per GPU (127.0.0.1 rendezvous), NCCL_DEBUG=INFO so
+    the communicator's rank count is visible; returns torchrun's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def barrier(ws):
@@ -220,7 +247,11 @@ def reassembly_ms(fn, ws, reps=5):
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / reps, ws)
-    return {"op": "ncclAllGather (torch.distributed all_gather_into_tensor)", "ms": round(ms, 4)}
+    import torch.distributed as dist
+    be = dist.get_backend()
+    op = "ncclAllGather" if be == "nccl" else f"{be} all-gather"
+    return {"op": f"{op} (torch.distributed all_gather_into_tensor / all_gather)", "backend": be,
+            "ms": round(ms, 4)}
 
 
 # ---------------------------------------------------------------------------
@@ -228,7 +259,8 @@ def reassembly_ms(fn, ws, reps=5):
 # ---------------------------------------------------------------------------
 def cpu_gemm_sample(seconds_target: float = 12.0):
     """Time oracle_gemm (oracles.cpp:14-26) on a row sample of the 8192^3
-    workload with all host threads; returns (TFLOP/s, threads, sample)."""
+    workload with all host threads (one row block each), plus the as-shipped
+    single-thread rate on a 2-row sample; returns a cpu_baseline dict."""
     import oracle
     R = oracle.REF
     kind = "reference"
@@ -237,12 +269,12 @@ def cpu_gemm_sample(seconds_target: float = 12.0):
     b = oracle.round_bf16(rng.uniform(-1, 1, (GEMM_K, GEMM_N)).astype(np.float32))
     rows = threads
     a = oracle.round_bf16(rng.uniform(-1, 1, (rows, GEMM_K)).astype(np.float32))
-    c = np.empty((rows, GEMM_N), np.float32)
 
-    def run(nr):
+    def run(nr, thr):
+        c = np.empty((nr, GEMM_N), np.float32)
         t0 = time.perf_counter()
         if R is not None:
-            R.ref_oracle_gemm_mt(a[:nr].copy(), b, c[:nr].copy(), nr, GEMM_N, GEMM_K, threads)
+            R.ref_oracle_gemm_mt(a[:nr].copy(), b, c, nr, GEMM_N, GEMM_K, thr)
         else:
             oracle.oracle_gemm(a[:nr], b)
         return time.perf_counter() - t0
@@ -250,25 +282,35 @@ def cpu_gemm_sample(seconds_target: float = 12.0):
     if R is None:
         kind, threads = "port", 1
         rows = 1
-    dt = run(rows)
+    dt = run(rows, threads)
     if R is not None and dt < seconds_target / 3:
         per = int(min(16, max(1, round(seconds_target / max(dt, 1e-3)))))
         rows = threads * per
         a = oracle.round_bf16(rng.uniform(-1, 1, (rows, GEMM_K)).astype(np.float32))
-        c = np.empty((rows, GEMM_N), np.float32)
-        dt = run(rows)
+        dt = run(rows, threads)
     flops = 2.0 * rows * GEMM_N * GEMM_K
-    return (flops / dt / 1e12, threads, kind,
-            f"{rows} of {GEMM_M} rows of the 8192^3 GEMM ({threads} threads, one row block each),"
-            f" {dt:.1f} s")
+    one = None
+    if R is not None and threads > 1:
+        dt1 = run(2, 1)
+        one = 2.0 * 2 * GEMM_N * GEMM_K / dt1 / 1e12
+    return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": kind,
+            "sample": f"{rows} of {GEMM_M} rows of the 8192^3 GEMM ({threads} threads, one row block each), "
+                      f"{dt:.1f} s; whole-GEMM time extrapolated x{GEMM_M / rows:.1f} (rows are independent, "
+                      "oracles.cpp:17-23)",
+            "extrapolation_factor": round(GEMM_M / rows, 2),
+            "single_thread_value": one,
+            "single_thread_sample": "2 rows, 1 thread (the reference as shipped is single-threaded)"}
 
 
-def cpu_attention_sample():
+def cpu_attention_sample(seq: int = 4096):
+    """Time oracle_attention (oracles.cpp:119-145) on `threads` causal heads of
+    [seq, 128] with all host threads (one head each); returns a cpu_baseline
+    dict in TFLOPS (causal FA FLOP convention)."""
     import oracle
     R = oracle.REF
     threads = os.cpu_count() or 1
     heads = threads
-    s, d = 2048, FA_D  # oracle cost grows as S^2: time S=2048 heads, scale by (8192/2048)^2
+    s, d = seq, FA_D
     rng = np.random.default_rng(31)
     q, k, v = (oracle.round_bf16(rng.uniform(-1, 1, (heads, s, d)).astype(np.float32))
                for _ in range(3))
@@ -282,7 +324,10 @@ def cpu_attention_sample():
         heads, threads, kind = 1, 1, "port"
     dt = time.perf_counter() - t0
     flops = 4.0 * heads * d * s * (s + 1) / 2
-    return flops / dt / 1e12, threads, kind, f"{heads} causal heads S={s} D={d}, {dt:.1f} s"
+    return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": kind,
+            "sample": f"{heads} causal heads S={s} D={d} ({threads} threads, one head each), {dt:.1f} s; "
+                      f"configs[3] has {FA_B * FA_H} heads of S={FA_S} (cost ~S^2: one S={FA_S} head = "
+                      f"{(FA_S / s) ** 2:.0f}x a sampled head)"}
 
 
 # ---------------------------------------------------------------------------
@@ -315,35 +360,53 @@ def bench_gemm(args, rank, ws, local):
     value = ws * flop * args.steps / secs / 1e12
     achieved = flop / per_launch / 1e12
 
+    # same-box cuBLAS (torch.mm on the same operands) for context
+    cublas = None
+    try:
+        csecs = timed(lambda: torch.mm(a, b, out=c), args.steps, args.warmup, ws, stream)
+        cublas = round(flop * args.steps / csecs / 1e12, 2)
+    except Exception as e:  # noqa: BLE001
+        cublas = f"unavailable: {type(e).__name__}"
+
     # end to end through the reference-facing C-ABI with HOST f32 buffers
-    # (mimw_b200_oracle_gemm: pinned H2D of A,B, bf16 staging, GEMM, D2H of C)
+    # (mimw_b200_oracle_gemm: H2D of A, B, bf16 staging, GEMM, D2H of C), with
+    # pageable buffers as the reference's Tile (std::vector, sim.hpp:13-26)
+    # and with pinned ones
     e2e = None
     if not args.no_e2e:
-        ha = a.float().cpu().pin_memory()
-        hb = b.float().cpu().pin_memory()
-        hc = torch.empty((GEMM_M, GEMM_N), dtype=torch.float32).pin_memory()
-        fp = P._fp
         import ctypes
+        fp = P._fp
+        ha_pg = a.float().cpu().numpy()
+        hb_pg = b.float().cpu().numpy()
+        hc_pg = np.empty((GEMM_M, GEMM_N), np.float32)
+        hc_pg.fill(0)  # touch the pages once (a caller's Tile is resident)
+        ha = torch.from_numpy(ha_pg).pin_memory()
+        hb = torch.from_numpy(hb_pg).pin_memory()
+        hc = torch.empty((GEMM_M, GEMM_N), dtype=torch.float32).pin_memory()
 
-        def e2e_step():
-            P._check(L.mimw_b200_oracle_gemm(ctypes.cast(ha.data_ptr(), fp),
-                                             ctypes.cast(hb.data_ptr(), fp),
-                                             ctypes.cast(hc.data_ptr(), fp), GEMM_M, GEMM_N,
-                                             GEMM_K, P.PREC_BF16))
+        def e2e_time(pa, pb, pc):
+            def e2e_step():
+                P._check(L.mimw_b200_oracle_gemm(ctypes.cast(pa, fp), ctypes.cast(pb, fp), ctypes.cast(pc, fp),
+                                                 GEMM_M, GEMM_N, GEMM_K, P.PREC_BF16))
+            for _ in range(2):
+                e2e_step()
+            barrier(ws)
+            n_e2e = max(3, min(10, args.steps // 4))
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                e2e_step()
+            return max_over_ranks((time.perf_counter() - t0) / n_e2e, ws)
 
-        for _ in range(2):
-            e2e_step()
-        barrier(ws)
-        n_e2e = max(3, min(10, args.steps // 10))
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            e2e_step()
-        dt = max_over_ranks((time.perf_counter() - t0) / n_e2e, ws)
-        e2e = {"value": round(ws * flop / dt / 1e12, 2), "unit": "TFLOPS",
+        dt_pg = e2e_time(ha_pg.ctypes.data, hb_pg.ctypes.data, hc_pg.ctypes.data)
+        dt_pin = e2e_time(ha.data_ptr(), hb.data_ptr(), hc.data_ptr())
+        e2e = {"value": round(ws * flop / dt_pg / 1e12, 2), "unit": "TFLOPS",
                "h2d_bytes_per_step": e2e_h2d_bytes(GEMM_M, GEMM_N, GEMM_K),
                "d2h_bytes_per_step": 4 * GEMM_M * GEMM_N,
                "api": "mimw_b200_oracle_gemm (host f32 Tiles, include/mimw_b200.h)",
-               "ms_per_step": round(dt * 1e3, 3)}
+               "ms_per_step": round(dt_pg * 1e3, 3),
+               "host_buffers": "pageable (numpy, as the reference's std::vector Tile)",
+               "pinned": {"value": round(ws * flop / dt_pin / 1e12, 2), "ms_per_step": round(dt_pin * 1e3, 3)},
+               "pageable": {"value": round(ws * flop / dt_pg / 1e12, 2), "ms_per_step": round(dt_pg * 1e3, 3)}}
 
     res = {
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws,
@@ -362,6 +425,7 @@ def bench_gemm(args, rank, ws, local):
                      "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
                      "frac_of_spec_2250": round(achieved / 2250.0, 4),
                      "traffic": traffic("gemm_bf16_8192"),
+                     "cublas_tflops_same_box": cublas,
                      "algorithmic_bytes_min": 2.0 * (GEMM_M * GEMM_K + GEMM_K * GEMM_N + GEMM_M * GEMM_N),
                      "algorithmic_flop_per_launch": flop},
         "e2e": e2e,
@@ -373,7 +437,11 @@ def bench_gemm(args, rank, ws, local):
 
 def bench_attention(args, rank, ws, local):
     """configs[3]: causal FA forward bf16 B=4 H=32 S=8192 D=128, batch x head
-    sharded over the ranks (strong scaling: each rank runs B*H/N heads)."""
+    sharded over the ranks (strong scaling: each rank runs B*H/N heads).
+    Timed for the full --steps; e2e through the host-f32 reference-signature
+    entries; the reference oracle_attention timed on the host cores; cuDNN
+    SDPA timed on the same inputs for context."""
+    import ctypes
     import torch
     import paper_2605_10905_b200 as P
     L = P.lib()
@@ -397,7 +465,7 @@ def bench_attention(args, rank, ws, local):
                                               lse.data_ptr(), my, 1, FA_S, FA_S, scale, args.fa_emu,
                                               0, None, sptr))
 
-    steps = max(3, args.steps // 5) if args.workload != "attention" else args.steps
+    steps = args.steps
     clk = Clocks(local)
     clk.start()
     secs = timed(step, steps, args.warmup, ws, stream)
@@ -407,10 +475,63 @@ def bench_attention(args, rank, ws, local):
     value = flop_total * steps / secs / 1e12
     achieved = flop_mine / (secs / steps) / 1e12
     reasm = None
-    if ws > 1:  # NCCL all-gather of O and LSE, reported beside (not inside) the compute number
+    if ws > 1:  # all-gather of O and LSE, reported beside (not inside) the compute number
         reasm = reassembly_ms(lambda: (shard.all_gather_rows(o, ranges),
                                        shard.all_gather_rows(lse, ranges)), ws)
         reasm["bytes_gathered"] = bh * FA_S * (FA_D * 2 + 4)
+    # cuDNN SDPA (torch) on the same inputs, same box, for context
+    cudnn = None
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+            f = lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)  # noqa: E731
+            cs = timed(f, steps, args.warmup, ws, stream)
+        cudnn = round(flop_total * steps / cs / 1e12, 2)
+    except Exception as e:  # noqa: BLE001
+        cudnn = f"unavailable: {type(e).__name__}"
+    # end to end through the host-f32 reference-signature entries, pageable
+    # numpy buffers (the reference's Tile): (a) the batched entry, all of this
+    # rank's heads in one call; (b) the per-head oracle_attention signature
+    # called once per head
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (t.reshape(my, FA_S, FA_D).float().cpu().numpy() for t in (q, k, v))
+        ho = np.zeros((my, FA_S, FA_D), np.float32)
+        hl = np.zeros((my, FA_S), np.float32)
+        fp = P._fp
+        cp = lambda x: ctypes.cast(x.ctypes.data, fp)  # noqa: E731
+
+        def batched():
+            P._check(L.mimw_b200_oracle_attention_heads(cp(hq), cp(hk), cp(hv), cp(ho), cp(hl), my, FA_S,
+                                                        FA_D, FA_S, scale, P.PREC_BF16))
+
+        def per_head():
+            for h in range(my):
+                P._check(L.mimw_b200_oracle_attention_ex(cp(hq[h]), cp(hk[h]), cp(hv[h]), cp(ho[h]), cp(hl[h]),
+                                                         FA_S, FA_D, FA_S, scale, P.PREC_BF16))
+
+        def wall(fn, n):
+            fn()
+            barrier(ws)
+            t0 = time.perf_counter()
+            for _ in range(n):
+                fn()
+            return max_over_ranks((time.perf_counter() - t0) / n, ws)
+
+        dt = wall(batched, max(3, min(10, args.steps // 4)))
+        dt_ph = wall(per_head, 2)
+        elems = my * FA_S * FA_D
+        e2e = {"value": round(flop_total / dt / 1e12, 2), "unit": "TFLOPS",
+               "h2d_bytes_per_step": 3 * 2 * my * FA_S * 128,
+               "d2h_bytes_per_step": 2 * my * FA_S * 128 + 4 * my * FA_S,
+               "ms_per_step": round(dt * 1e3, 3),
+               "api": "mimw_b200_oracle_attention_heads (host f32 [H,S,D], pageable numpy; f32<->bf16 on "
+                      "host threads, PCIe at 2 B/element)",
+               "host_f32_bytes_per_step": 4 * 4 * elems,
+               "per_head_reference_signature": {
+                   "value": round(flop_total / dt_ph / 1e12, 2), "ms_per_step": round(dt_ph * 1e3, 3),
+                   "api": f"mimw_b200_oracle_attention_ex called {my} times (one [S,D] head per call, "
+                          "the reference's oracle_attention signature)"}}
     res = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws,
            "steps": steps, "warmup": args.warmup, "ms_per_step": round(secs / steps * 1e3, 4),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -426,8 +547,9 @@ def bench_attention(args, rank, ws, local):
                         "frac_of_spec_2250": round(achieved / 2250.0, 4),
                         "peak_source": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json)",
                         "traffic": traffic("attention_fwd_b4h32s8192") if ws == 1 else None,
-                        "algorithmic_flop_per_launch": flop_mine},
-           "gpu_launches": steps, "clocks": clocks}
+                        "algorithmic_flop_per_launch": flop_mine,
+                        "cudnn_sdpa_tflops_same_box": cudnn},
+           "e2e": e2e, "gpu_launches": steps, "clocks": clocks}
     return res
 
 
@@ -834,7 +956,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gemm", choices=["gemm", "attention", "fp8", "moe", "layernorm", "simplicial",
-                             "multidevice", "attention_bwd"])
+                             "multidevice", "attention_bwd", "launchcheck"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -847,29 +969,48 @@ def main():
         if rank != 0:
             return
         vals, info = [], None
-        for _ in range(args.warmup and 1):
-            pass
         for _ in range(max(1, args.steps)):
-            v, thr, kind, sample = cpu_gemm_sample()
-            vals.append(v)
-            info = (thr, kind, sample)
+            info = cpu_gemm_sample()
+            vals.append(info["value"])
             if len(vals) >= 3:  # each step is a bounded sample; keep the run to minutes
                 break
         v = float(np.median(vals))
+        fa = cpu_attention_sample()
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS",
                "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": len(vals),
                "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                "dtype": "f32", "data": "synthetic U[-1,1] rounded to bf16",
                "config": {"workload": "configs[1] GEMM 8192^3 via reference oracle_gemm "
                                       "(oracles.cpp:14-26) on host cores, row-sampled"},
-               "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": info[0], "kind": info[1],
-                                "sample": info[2]},
+               "cpu_baseline": dict(info, value=v),
                "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0}}
+                       "d2h_bytes_per_step": 0},
+               "fa_fwd": {"value": fa["value"], "unit": "TFLOPS",
+                          "config": {"workload": "configs[3] causal attention via reference oracle_attention "
+                                                 "(oracles.cpp:119-145) on host cores, head-sampled"},
+                          "cpu_baseline": fa}}
         print(json.dumps(out))
         return
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     rank, ws, local = dist_init(args.gpus)
+    fa = None
+    if args.workload == "launchcheck":
+        # the multi-rank launch path alone (no kernels): tests/test_bench_launch.py
+        import torch.distributed as dist
+        t = np.array([rank], dtype=np.int64)
+        if ws > 1:
+            import torch
+            tt = torch.tensor([rank], dtype=torch.int64)
+            dist.all_reduce(tt)
+            t = tt.numpy()
+        if rank == 0:
+            print(json.dumps({"workload": "launchcheck", "n_gpus": ws, "rank_sum": int(t[0]),
+                              "backend": dist.get_backend() if ws > 1 else None}))
+        if ws > 1:
+            dist.destroy_process_group()
+        return
     if args.workload == "attention":
         res = bench_attention(args, rank, ws, local)
     elif args.workload == "fp8":
@@ -888,10 +1029,8 @@ def main():
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
             fa = bench_attention(args, rank, ws, local)
-            res["secondary"] = {"attention_fwd": {k: fa[k] for k in (
-                "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks",
-                "reassembly")}}
-            res["secondary"]["mxfp8_gemm"] = bench_mxfp8(args, rank, ws, local)
+            torch_empty_cache()
+            res["secondary"] = {"mxfp8_gemm": bench_mxfp8(args, rank, ws, local)}
             torch_empty_cache()
             moe = bench_moe(args, rank, ws, local)
             res["secondary"]["grouped_moe_gemm"] = {k: moe[k] for k in (
@@ -904,17 +1043,28 @@ def main():
             res["secondary"]["attention_bwd"] = bench_attention_bwd(args, rank, ws, local)
             torch_empty_cache()
             try:
-                if ws > 1 and not os.environ.get("MIMW_BENCH_MD"):
-                    # real peers need every rank's kernel in the device barrier: opt-in
-                    # (--workload multidevice or MIMW_BENCH_MD=1) so the scaling line is never at risk
-                    raise RuntimeError("multi-GPU form: run --workload multidevice")
+                if ws > 1 and os.environ.get("MIMW_BENCH_MD", "1") == "0":
+                    raise RuntimeError("disabled by MIMW_BENCH_MD=0")
+                if ws > 1 and backend_for(ws) != "nccl":
+                    # ranks sharing one GPU cannot meet in the device-side barrier
+                    # (kernels of different processes do not run concurrently)
+                    raise RuntimeError("skipped: ranks share a GPU (gloo functional run)")
+                if ws > 1:
+                    # real peers: a straggler is waited for at most this long (device-side barrier)
+                    os.environ.setdefault("MIMW_PEER_WAIT_S", "60")
                 res["secondary"]["multi_device_gemm"] = bench_multidevice(args, rank, ws, local)
             except Exception as e:  # never lose the headline line to the §8f extra
                 res["secondary"]["multi_device_gemm"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, thr, kind, sample = cpu_gemm_sample()
-        res["cpu_baseline"] = {"value": v, "unit": "TFLOPS", "cores": thr, "kind": kind,
-                               "sample": sample}
+        res["cpu_baseline"] = cpu_attention_sample() if args.workload == "attention" else cpu_gemm_sample()
+        if fa is not None:
+            fa["cpu_baseline"] = cpu_attention_sample()
+    if fa is not None:
+        # FA-fwd (the other half of BASELINE's metric) as the LAST key of the
+        # line, so it is in any captured tail of stdout
+        res["fa_fwd"] = {k: fa[k] for k in ("value", "unit", "ms_per_step", "steps", "scaling", "config",
+                                            "roofline", "clocks", "e2e", "cpu_baseline", "reassembly",
+                                            "gpu_launches") if k in fa}
     if rank == 0:
         print(json.dumps(res))
     if ws > 1:

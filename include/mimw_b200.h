@@ -54,6 +54,13 @@ extern "C" {
 int mimw_b200_version(void);
 const char *mimw_b200_last_error(void);
 
+/* Device scratch (staging buffers, the attention-backward dQ accumulator)
+ * comes from a library-private stream-ordered memory pool per device that
+ * keeps freed memory for the next call; the device's default pool is never
+ * modified.  This returns the private pool's cached memory of the current
+ * device to the driver. */
+int mimw_b200_trim_pool(void);
+
 /* ---- GEMM:  C[M,N] = A[M,K] . B  (fp32 accumulate in TMEM) ----------------
  * Replaces: Tile oracle_gemm(const Tile &a, const Tile &b)
  *           proj/core/include/mimw/oracles.hpp:15-16 (oracles.cpp:14-26).
@@ -168,6 +175,15 @@ int mimw_b200_ipc_free(void *ptr);
  * as oracle_simplicial_attention's lse, oracles.cpp:116) may be NULL. */
 int mimw_b200_oracle_attention(const float *q, const float *k, const float *v, float *o,
                                float *lse, int64_t seq, int64_t d, int64_t w, double scale);
+
+/* Batched form for `heads` independent heads stored back to back: q, k, v, o
+ * host f32 [heads, seq, d], lse [heads, seq] or NULL; head h is exactly
+ * oracle_attention(q[h], k[h], v[h], w, scale).  No reference counterpart
+ * (the reference's callers loop over heads); one call pipelines the heads
+ * through PCIe and the B200 kernel.  precision as mimw_b200_oracle_attention_ex. */
+int mimw_b200_oracle_attention_heads(const float *q, const float *k, const float *v, float *o,
+                                     float *lse, int64_t heads, int64_t seq, int64_t d, int64_t w,
+                                     double scale, int32_t precision);
 
 /* window value selecting non-causal attention (every key of the sequence; the
  * paper's AFN / ABC rows, PAPER.md:702-716 — no reference oracle) */

@@ -52,6 +52,11 @@ def _declare_c(lib):
     lib.orc_gemm.argtypes = [_f32p, _f32p, _f32p, _i64, _i64, _i64]
     lib.orc_gemm_rows.argtypes = [_f32p, _f32p, _f32p, _i64, _i64, _i64, _i64, _i64]
     lib.orc_multi_device_gemm.argtypes = [_f32p] * 5 + [_i64] * 4
+    lib.orc_gemm_rowlist_mt.argtypes = [_f32p, _f32p, _f32p, _i64, _i64, _i64, C_.c_int]
+    lib.orc_attention_rowlist_mt.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p, _i64, _i64, _i64,
+                                             C_.c_int, C_.c_double,
+                                             np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"),
+                                             _i64, C_.c_int]
     lib.orc_attention.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p,
                                   _i64, _i64, _i64, C_.c_double]
     lib.orc_attention_rows.argtypes = [_f32p, _f32p, _f32p, _f32p, C_.c_void_p,
@@ -167,6 +172,34 @@ def oracle_gemm(a, b, rows=None) -> np.ndarray:
     full = np.zeros((m, n), np.float32)
     C.orc_gemm_rows(a, b, full, m, n, k, r0, r1)
     return full[r0:r1]
+
+
+def oracle_gemm_rowlist(a_rows, b, threads: int | None = None) -> np.ndarray:
+    """Rows of C = A.B given the gathered rows ``a_rows`` [R, K] of A and B
+    [K, N]: the reference's arithmetic (oracles.cpp:17-23, float accumulator,
+    ascending k) restated with a cache-friendly loop order and threads;
+    bit-identical to oracle_gemm (tests/test_oracle.py)."""
+    a, b = _f32(a_rows), _f32(b)
+    r, k = a.shape
+    n = b.shape[1]
+    c = np.empty((r, n), np.float32)
+    C.orc_gemm_rowlist_mt(a, b, c, r, n, k, threads or (os.cpu_count() or 1))
+    return c
+
+
+def oracle_attention_rowlist(q, k, v, w: int, scale: float, rows, causal: bool = True,
+                             threads: int | None = None):
+    """Sparse rows of one head's attention (oracles.cpp:119-145; causal=False:
+    the restated every-key variant), threaded: returns (o[len(rows), D],
+    lse[len(rows)])."""
+    q, k, v = map(_f32, (q, k, v))
+    s, d = q.shape
+    rr = np.ascontiguousarray(np.asarray(rows, np.int64))
+    o = np.empty((len(rr), d), np.float32)
+    lse = np.empty(len(rr), np.float32)
+    C.orc_attention_rowlist_mt(q, k, v, o, lse.ctypes.data, s, d, w, 1 if causal else 0, scale, rr, len(rr),
+                               threads or (os.cpu_count() or 1))
+    return o, lse
 
 
 def oracle_grouped_gemm(x, m_offsets, w, rows=None) -> list:

@@ -18,6 +18,7 @@
  * `s += a*b`, which g++ -O3 without -march never contracts).
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -179,6 +180,62 @@ void orc_gemm(const float *a, const float *b, float *c, int64_t m, int64_t n,
   orc_gemm_rows(a, b, c, m, n, k, 0, m);
 }
 
+/* Selected rows of C = A.B for config-scale parity: c[r, :] = a[r, :] . B for
+ * the R rows given as a[R, K] (gathered by the caller), B [K, N] row-major.
+ * Same arithmetic as oracles.cpp:17-23 — per element a float accumulator
+ * starting at 0.0f, s += a[k]*b[k][j] in ascending k, no FMA contraction —
+ * so bit-identical to the reference (tests/test_oracle.py pins it), but the
+ * loop runs k-outer over a block of rows and a slice of columns per thread,
+ * streaming B row-contiguously (vectorised across j), so 8192^3-scale row
+ * samples take seconds instead of the reference's strided walk. */
+typedef struct {
+  const float *a, *b;
+  float *c;
+  int64_t R, N, K, j0, j1;
+} rowlist_job;
+
+static void *gemm_rowlist_worker(void *arg) {
+  const rowlist_job *jb = (const rowlist_job *)arg;
+  const int64_t RB = 16, JB = 512;
+  float acc[16 * 512];
+  for (int64_t r0 = 0; r0 < jb->R; r0 += RB) {
+    const int64_t rn = jb->R - r0 < RB ? jb->R - r0 : RB;
+    for (int64_t j0 = jb->j0; j0 < jb->j1; j0 += JB) {
+      const int64_t jn = jb->j1 - j0 < JB ? jb->j1 - j0 : JB;
+      for (int64_t x = 0; x < rn * JB; ++x) acc[x] = 0.0f;
+      for (int64_t kk = 0; kk < jb->K; ++kk) {
+        const float *br = jb->b + kk * jb->N + j0;
+        for (int64_t r = 0; r < rn; ++r) {
+          const float av = jb->a[(r0 + r) * jb->K + kk];
+          float *ar = acc + r * JB;
+          for (int64_t j = 0; j < jn; ++j) ar[j] = ar[j] + av * br[j];
+        }
+      }
+      for (int64_t r = 0; r < rn; ++r)
+        memcpy(jb->c + (r0 + r) * jb->N + j0, acc + r * JB, sizeof(float) * (size_t)jn);
+    }
+  }
+  return NULL;
+}
+
+void orc_gemm_rowlist_mt(const float *a, const float *b, float *c, int64_t R, int64_t N, int64_t K,
+                         int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  rowlist_job jobs[256];
+  const int64_t per = ((N + threads - 1) / threads + 7) / 8 * 8;
+  int nt = 0;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t j0 = t * per, j1 = j0 + per < N ? j0 + per : N;
+    if (j0 >= j1) break;
+    jobs[nt] = (rowlist_job){a, b, c, R, N, K, j0, j1};
+    pthread_create(&th[nt], NULL, gemm_rowlist_worker, &jobs[nt]);
+    ++nt;
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
 /* Gathered GEMM: A = [a0 | a1], B = [b0 ; b1] (core/src/oracles.cpp:57-80). */
 void orc_multi_device_gemm(const float *a0, const float *a1, const float *b0,
                            const float *b1, float *c, int64_t m, int64_t k0,
@@ -283,6 +340,45 @@ void orc_attention_mode_rows(const float *q, const float *k, const float *v, flo
     if (lse) lse[i] = (float)(m + log(l));
   }
   free(scores);
+}
+
+/* Sparse rows of one head's attention (rows[] in any order, each computed as
+ * orc_attention_mode_rows(row, row + 1)), spread over pthreads; o[nrows, d],
+ * lse[nrows].  For config-scale parity (one row per work item). */
+typedef struct {
+  const float *q, *k, *v;
+  float *o, *lse;
+  int64_t seq, d, w;
+  int causal;
+  double scale;
+  const int64_t *rows;
+  int64_t i0, i1;
+} attn_rows_job;
+
+static void *attn_rows_worker(void *arg) {
+  const attn_rows_job *jb = (const attn_rows_job *)arg;
+  for (int64_t i = jb->i0; i < jb->i1; ++i)
+    orc_attention_mode_rows(jb->q, jb->k, jb->v, jb->o + i * jb->d, jb->lse ? jb->lse + i : NULL, jb->seq,
+                            jb->d, jb->w, jb->causal, jb->scale, jb->rows[i], jb->rows[i] + 1);
+  return NULL;
+}
+
+void orc_attention_rowlist_mt(const float *q, const float *k, const float *v, float *o, float *lse,
+                              int64_t seq, int64_t d, int64_t w, int causal, double scale,
+                              const int64_t *rows, int64_t nrows, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  attn_rows_job jobs[256];
+  int nt = 0;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t i0 = nrows * t / threads, i1 = nrows * (t + 1) / threads;
+    if (i0 >= i1) continue;
+    jobs[nt] = (attn_rows_job){q, k, v, o, lse, seq, d, w, causal, scale, rows, i0, i1};
+    pthread_create(&th[nt], NULL, attn_rows_worker, &jobs[nt]);
+    ++nt;
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
 }
 
 /* Attention backward for one head: the gradients of o = softmax(scale q k^T) v

@@ -73,6 +73,9 @@ def _optional_sigs():
         "mimw_b200_oracle_attention": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double],
         "mimw_b200_oracle_attention_ex": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, C.c_double,
                                           C.c_int32],
+        "mimw_b200_oracle_attention_heads": [_fp, _fp, _fp, _fp, _fp, _i64, _i64, _i64, _i64,
+                                             C.c_double, C.c_int32],
+        "mimw_b200_trim_pool": [],
         "mimw_b200_oracle_simplicial_attention_ex": [_fp] * 7 + [_i64] * 4 + [C.c_double, C.c_int32],
         "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_bwd": [_vp] * 5 + [_vp] + [_vp] * 3 + [_i64] * 5 + [C.c_double, _vp],
@@ -145,12 +148,36 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False,
     if not hasattr(L, "mimw_b200_oracle_attention"):
         raise MimwError(ERR_UNSUPPORTED, "attention not built")
     q, k, v = map(_f32, (q, k, v))
+    if q.ndim != 2 or k.shape != q.shape or v.shape != q.shape:
+        raise MimwError(ERR_SHAPE, "q, k, v must be [S, D] of one shape")
     s, d = q.shape
     o = np.empty((s, d), np.float32)
     lse = np.empty(s, np.float32)
     _check(L.mimw_b200_oracle_attention_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s, d, w,
                                            scale, precision))
     return (o, lse) if with_lse else o
+
+
+def oracle_attention_heads(q, k, v, w: int, scale: float, with_lse: bool = False,
+                           precision: int = PREC_BF16):
+    """``oracle_attention`` for ``H`` independent heads in one call: q, k, v
+    float32 [H, S, D]; head h equals ``oracle_attention(q[h], k[h], v[h], w,
+    scale)``.  The heads are pipelined through PCIe and the B200 kernel
+    (mimw_b200_oracle_attention_heads)."""
+    q, k, v = map(_f32, (q, k, v))
+    if q.ndim != 3 or k.shape != q.shape or v.shape != q.shape:
+        raise MimwError(ERR_SHAPE, "q, k, v must be [H, S, D] of one shape")
+    h, s, d = q.shape
+    o = np.empty((h, s, d), np.float32)
+    lse = np.empty((h, s), np.float32)
+    _check(lib().mimw_b200_oracle_attention_heads(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), h, s, d,
+                                                  w, scale, precision))
+    return (o, lse) if with_lse else o
+
+
+def trim_pool() -> None:
+    """Return the library's cached device scratch to the driver."""
+    _check(lib().mimw_b200_trim_pool())
 
 
 def oracle_simplicial_attention(q, k1, v1, k2, v2, w1: int, w2: int, scale: float,
@@ -194,10 +221,11 @@ def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: 
     if name == "multi_device_gemm":
         return {"c": oracle_multi_device_gemm(inputs["a0"], inputs["a1"], inputs["b0"],
                                               inputs["b1"], gp)}
-    if name == "simplicial_attention":
+    if name == "simplicial_attention":  # scalar defaults as sc("w1", 2) ... (oracles.cpp:190-193)
         o, lse = oracle_simplicial_attention(inputs["q"], inputs["k1"], inputs["v1"], inputs["k2"],
-                                             inputs["v2"], int(scalars["w1"]), int(scalars["w2"]),
-                                             scalars["scale"], PREC_F32 if precision else PREC_BF16)
+                                             inputs["v2"], int(scalars.get("w1", 2)),
+                                             int(scalars.get("w2", 16)), scalars.get("scale", 1.0),
+                                             PREC_F32 if precision else PREC_BF16)
         return {"o": o, "lse": lse}
     if name == "layernorm":
         return {"y": oracle_layernorm(inputs["x"], inputs["w"], inputs["b"],
@@ -212,6 +240,16 @@ def run_oracle(name: str, inputs: dict, scalars: dict | None = None, precision: 
 # ---------------------------------------------------------------------------
 # device path (torch CUDA tensors as plumbing)
 # ---------------------------------------------------------------------------
+def _need(t, dtype, what: str, ndim: int):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise MimwError(ERR_ARG, f"{what}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise MimwError(ERR_UNSUPPORTED, f"{what}: dtype {t.dtype}, expected {dtype}")
+    if t.dim() != ndim:
+        raise MimwError(ERR_SHAPE, f"{what}: expected {ndim} dims, got shape {tuple(t.shape)}")
+
+
 def _stream(stream):
     import torch
     return _vp(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
@@ -222,8 +260,23 @@ def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_
     """C = A.B with bf16 A [M,K], B [K,N] (B_KN) or [N,K] (B_NK); fp32 accumulate.
     ``out`` dtype float32 or bfloat16."""
     import torch
+    _need(a, torch.bfloat16, "gemm a", 2)
+    _need(b, torch.bfloat16, "gemm b", 2)
+    if b_layout not in (B_KN, B_NK):
+        raise MimwError(ERR_ARG, "bad b_layout")
     m, k = a.shape
-    n = b.shape[1] if b_layout == B_KN else b.shape[0]
+    kb, n = (b.shape[0], b.shape[1]) if b_layout == B_KN else (b.shape[1], b.shape[0])
+    if kb != k:
+        raise MimwError(ERR_SHAPE, f"dot conformance: a.shape[1]={k} != K of b={kb}")
+    for t, nm in ((a, "a"), (b, "b")):
+        if t.stride(1) != 1:
+            raise MimwError(ERR_UNSUPPORTED, f"gemm {nm}: rows must be contiguous")
+    if out is not None:
+        if out.dtype not in (torch.float32, torch.bfloat16) or tuple(out.shape) != (m, n) \
+                or out.stride(1) != 1 or out.device != a.device:
+            raise MimwError(ERR_SHAPE, f"gemm out: need an f32/bf16 [{m}, {n}] tensor with contiguous rows")
+    if b.device != a.device:
+        raise MimwError(ERR_ARG, "gemm: a and b on different devices")
     if out is None:
         out = torch.empty((m, n), device=a.device, dtype=out_dtype or torch.bfloat16)
     cd = F32 if out.dtype == torch.float32 else BF16
@@ -243,7 +296,16 @@ def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None
     attention forward on bf16 [B, H, S, 128] CUDA tensors.  Returns (o, lse)
     with lse fp32 [B, H, S] (natural log)."""
     import torch
+    for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+        _need(t, torch.bfloat16, f"attention_fwd {nm}", 4)
+    if k.shape != q.shape or v.shape != q.shape:
+        raise MimwError(ERR_SHAPE, "attention_fwd: q, k, v must have one [B, H, S, D] shape")
     b, h, s, d = q.shape
+    if out is not None and (out.shape != q.shape or out.dtype != torch.bfloat16):
+        raise MimwError(ERR_SHAPE, "attention_fwd: out must be a bf16 tensor of q's shape")
+    if lse is not None and (tuple(lse.shape) != (b, h, s) or lse.dtype != torch.float32
+                            or not lse.is_contiguous()):
+        raise MimwError(ERR_SHAPE, "attention_fwd: lse must be a contiguous f32 [B, H, S] tensor")
     if not causal:
         window = WINDOW_NONCAUSAL
     if out is None:
@@ -312,9 +374,19 @@ def layernorm(x, w, b, eps: float = 1e-5, out=None, mean=None, rstd=None, stream
               cluster: int = 0):
     """Cluster LayerNorm over the last dim of an f32 CUDA tensor [rows, n]."""
     import torch
-    if x.dtype != torch.float32 or not x.is_contiguous():
+    _need(x, torch.float32, "layernorm x", 2)
+    if not x.is_contiguous():
         raise MimwError(ERR_UNSUPPORTED, "layernorm needs a contiguous float32 tensor")
     rows, n = x.shape
+    for t, nm in ((w, "w"), (b, "b")):
+        _need(t, torch.float32, f"layernorm {nm}", 1)
+        if t.numel() < n or not t.is_contiguous():
+            raise MimwError(ERR_SHAPE, f"layernorm {nm}: need a contiguous f32 vector of >= {n} elements")
+    for t, nm in ((mean, "mean"), (rstd, "rstd")):
+        if t is not None and (t.dtype != torch.float32 or t.numel() < rows or not t.is_contiguous()):
+            raise MimwError(ERR_SHAPE, f"layernorm {nm}: need a contiguous f32 vector of >= {rows} elements")
+    if out is not None and (out.shape != x.shape or out.dtype != torch.float32 or not out.is_contiguous()):
+        raise MimwError(ERR_SHAPE, "layernorm out: need a contiguous f32 tensor of x's shape")
     if out is None:
         out = torch.empty_like(x)
     _check(lib().mimw_b200_layernorm_ex(x.data_ptr(), w.data_ptr(), b.data_ptr(), out.data_ptr(),

@@ -522,9 +522,8 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
   // [bh, npad] f32
   const size_t acc_bytes = (size_t)bh * D * npad * 4;
   const size_t vec_bytes = (size_t)bh * npad * 4;
-  keep_pool_memory();  // stream-ordered scratch, pool keeps its memory (pool.h)
   char *ws = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&ws), acc_bytes + 2 * vec_bytes + 256, stream);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void **>(&ws), acc_bytes + 2 * vec_bytes + 256, stream);
   if (e != cudaSuccess) return e;
   float *acc = reinterpret_cast<float *>(ws);
   float *lse2 = reinterpret_cast<float *>(ws + acc_bytes);

@@ -110,7 +110,9 @@ attention_f32_kernel(const float *__restrict__ q, const float *__restrict__ k1, 
 cudaError_t attention_f32_launch(const AttnF32Args &a, cudaStream_t stream) {
   if (a.seq <= 0) return cudaSuccess;
   attention_f32_kernel<<<(unsigned)a.seq, THREADS, 0, stream>>>(
-      a.q, a.k1, a.v1, a.k2, a.v2, a.o, a.lse, (int)a.seq, (int)a.d, (int)a.w1, (int)a.w2, a.causal ? 1 : 0,
+      a.q, a.k1, a.v1, a.k2, a.v2, a.o, a.lse, (int)a.seq, (int)a.d,
+      (int)(a.w1 < a.seq ? a.w1 : a.seq), (int)(a.w2 < a.seq ? a.w2 : a.seq),  // windows >= seq: every key (no int overflow)
+      a.causal ? 1 : 0,
       a.simplicial ? 1 : 0, a.scale);
   return cudaGetLastError();
 }

@@ -39,7 +39,9 @@
 #include "pool.h"
 #include "tma_host.h"
 
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 
 namespace mimw {
 
@@ -79,7 +81,7 @@ struct Params {
   float *lse;        // [bh, seq] or null
   __nv_bfloat16 *o;  // [bh, seq, 128]
   int scale_pos;     // scale > 0: max on raw scores, scale folded into FFMA2
-  int *work_counter; // dynamic scheduler counter (zeroed before launch)
+  int *work_counter; // {claims, retired}: dynamic scheduler counter, zeroed by the last CTA
   unsigned long long *trace;  // optional per-warp cycle accounting [grid][12][8]
   int dbg;           // timing-only probes (MIMW_FA_DEBUG): 1 = skip the O stores
 };
@@ -183,7 +185,18 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mbar_wait(sched_empty(ss), ((n >> 1) & 1) ^ 1, 12);
         sched_slot[ss] = it < num_items ? it : -1;
         mbar_arrive(sched_full(ss));
-        if (it >= num_items) break;
+        if (it >= num_items) {
+          // self-reset of this launch's counter slot: the last CTA to retire
+          // (after every CTA's final claim, fenced) zeroes it for the next
+          // launch that draws the slot
+          __threadfence();
+          if (atomicAdd(p.work_counter + 1, 1) == (int)gridDim.x - 1) {
+            p.work_counter[0] = 0;
+            p.work_counter[1] = 0;
+            __threadfence();
+          }
+          break;
+        }
         int bh, qb;
         work_item(it, p, bh, qb);
         const int r0 = qb * 2 * BQ;
@@ -587,6 +600,26 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   }
 }
 
+constexpr int kCounterSlots = 1024;
+
+int *fa_counter_slot() {
+  static std::once_flag once[64];
+  static int *ring[64] = {};
+  static std::atomic<uint32_t> next[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::call_once(once[dev], [dev] {
+    int *r = nullptr;
+    if (cudaMalloc(&r, sizeof(int) * 2 * kCounterSlots) == cudaSuccess &&
+        cudaMemset(r, 0, sizeof(int) * 2 * kCounterSlots) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess)
+      ring[dev] = r;
+    else
+      cudaGetLastError();
+  });
+  if (!ring[dev]) return nullptr;
+  return ring[dev] + 2 * (next[dev].fetch_add(1) % kCounterSlots);
+}
+
 }  // namespace
 
 cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
@@ -616,12 +649,12 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   int grid = sm_count();
   if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
   if (grid > items) grid = items;
-  // The scheduler counter is per launch, stream-ordered scratch: launches on
-  // different streams (or host threads) never share it.
-  keep_pool_memory();
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p.work_counter), sizeof(int), stream);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
+  // Scheduler counter: a slot of a per-device ring of zeroed {claims, retired}
+  // pairs, drawn round-robin per launch, so launches on different streams or
+  // host threads never share one while in flight; the kernel's last CTA
+  // zeroes its slot (no per-launch allocation or memset).
+  p.work_counter = fa_counter_slot();
+  cudaError_t e = p.work_counter ? cudaSuccess : cudaErrorMemoryAllocation;
   auto launch = [&](auto kern) {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e2 != cudaSuccess) return e2;
@@ -637,8 +670,7 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
       default: e = launch(attention_fwd_kernel<4>); break;
     }
   }
-  const cudaError_t e3 = cudaFreeAsync(p.work_counter, stream);
-  return e != cudaSuccess ? e : e3;
+  return e;
 }
 
 }  // namespace mimw

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -97,15 +98,31 @@ struct Event {
   Event(Event &&o) noexcept : e(o.e) { o.e = nullptr; }
 };
 
-// Per-thread, per-device copy streams for the pipelined host-buffer entries.
+// Per-thread, per-device copy streams for the pipelined host-buffer entries,
+// destroyed when the thread exits.
+struct SideStreams {
+  cudaStream_t st[64][2] = {};
+  ~SideStreams() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (int d = 0; d < 64; ++d)
+      if (st[d][0] || st[d][1]) {
+        cudaSetDevice(d);
+        for (auto &x : st[d])
+          if (x) cudaStreamDestroy(x);
+      }
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+};
+
 cudaStream_t side_stream(int which) {
-  thread_local cudaStream_t st[64][2] = {};
+  thread_local SideStreams ss;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (!st[dev][which])
-    check_cuda(cudaStreamCreateWithFlags(&st[dev][which], cudaStreamNonBlocking), "stream create");
-  return st[dev][which];
+  if (!ss.st[dev][which])
+    check_cuda(cudaStreamCreateWithFlags(&ss.st[dev][which], cudaStreamNonBlocking), "stream create");
+  return ss.st[dev][which];
 }
 
 // RAII device scratch on a stream.
@@ -113,8 +130,7 @@ struct DevBuf {
   void *p = nullptr;
   cudaStream_t s;
   DevBuf(size_t bytes, cudaStream_t st) : s(st) {
-    mimw::keep_pool_memory();
-    if (bytes) check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    if (bytes) check_cuda(mimw::scratch_alloc(&p, bytes, s), "scratch allocation (private pool)");
   }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);
@@ -123,15 +139,41 @@ struct DevBuf {
   T *as() const { return static_cast<T *>(p); }
 };
 
+// Synchronizes the side streams when a host entry unwinds on an error, before
+// its DevBufs (declared earlier, destroyed later) free device scratch that an
+// in-flight copy on cs / ds may still touch, and before the thread's pinned
+// slots can be refilled by the next call.
+struct UnwindSync {
+  cudaStream_t st[3];
+  int n0;
+  UnwindSync(cudaStream_t a, cudaStream_t b, cudaStream_t c) : st{a, b, c}, n0(std::uncaught_exceptions()) {}
+  ~UnwindSync() {
+    if (std::uncaught_exceptions() > n0)
+      for (auto x : st) cudaStreamSynchronize(x);
+  }
+};
+
 // MIMW_PREC_BF16 path of host_gemm with the f32 -> bf16 rounding done on the
 // host threads (host_stage.h) straight into the device layout in pinned
 // slots: PCIe carries 2 bytes per input element instead of 4, and the
 // conversion of chunk i+1 overlaps the DMA of chunk i.  Same bf16 values as
 // the device staging kernels, so the results are bit-identical.
+// A host pointer the DMA engines can use directly (pinned / registered /
+// managed)?  Pageable memory (a std::vector Tile, a numpy array) is instead
+// read and written by the host threads through pinned slots.
+static bool dma_capable(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type != cudaMemoryTypeUnregistered;
+}
+
 static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
                                   const std::vector<const float *> &b_parts, const std::vector<int64_t> &k_parts,
                                   int64_t m, int64_t n, int64_t k, float *c, cudaStream_t s, cudaStream_t cs,
-                                  cudaStream_t ds, int mode) {
+                                  cudaStream_t ds, int mode, bool c_pageable) {
   // mode 1: every chunk rounded on the host; 2: B's odd row chunks (and all of
   // A) go over PCIe as f32 and are rounded by the device staging kernels, so
   // the host threads and the H2D stream share B's transfer; 3: also A's odd
@@ -140,6 +182,7 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
   const int64_t np = round_up(n, 8);
   DevBuf dA(2 * m * kp, s), dB(2 * kp * np, s), dC(sizeof(float) * m * np, s);
   DevBuf dF(mode == 1 ? 0 : sizeof(float) * (m + n) * k, s);  // f32 landing for device-rounded chunks
+  UnwindSync guard(s, cs, ds);
   float *dFb = dF.as<float>(), *dFa = dF.as<float>() ? dF.as<float>() + (size_t)k * n : nullptr;
   Event e_alloc, e_b;
   check_cuda(cudaEventRecord(e_alloc.e, s), "event");
@@ -203,7 +246,15 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
   check_cuda(cudaEventRecord(e_b.e, cs), "event");
   check_cuda(cudaStreamWaitEvent(s, e_b.e, 0), "wait");
   const int nchunks = (int)((m + achunk - 1) / achunk);
-  std::vector<Event> e_a(nchunks), e_c(nchunks);
+  std::vector<Event> e_a(nchunks), e_c(nchunks), e_d(c_pageable ? nchunks : 0);
+  auto drain = [&](int ci) {
+    const int64_t r0 = ci * achunk, rows = std::min(achunk, m - r0);
+    check_cuda(cudaEventSynchronize(e_d[ci].e), "gemm execution");
+    const float *hc = static_cast<const float *>(mimw::pinned_slot(7 + (ci & 1), (size_t)achunk * n * 4));
+    mimw::host_parallel_for(rows, [&](int64_t lo, int64_t hi) {
+      std::memcpy(c + (r0 + lo) * n, hc + lo * n, sizeof(float) * (size_t)(hi - lo) * n);
+    });
+  };
   for (int ci = 0; ci < nchunks; ++ci) {
     const int64_t r0 = ci * achunk, rows = std::min(achunk, m - r0);
     char *dA_rows = static_cast<char *>(dA.p) + (size_t)r0 * kp * 2;
@@ -250,10 +301,23 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
     check_cuda(mimw::gemm_bf16_launch(g, s), "gemm launch");
     check_cuda(cudaEventRecord(e_c[ci].e, s), "event");
     check_cuda(cudaStreamWaitEvent(ds, e_c[ci].e, 0), "wait");
-    check_cuda(cudaMemcpy2DAsync(c + r0 * n, sizeof(float) * n, static_cast<char *>(dC.p) + (size_t)r0 * np * 4,
+    if (!c_pageable) {
+      check_cuda(cudaMemcpy2DAsync(c + r0 * n, sizeof(float) * n, static_cast<char *>(dC.p) + (size_t)r0 * np * 4,
+                                   sizeof(float) * np, sizeof(float) * n, rows, cudaMemcpyDeviceToHost, ds),
+                 "D2H c");
+      continue;
+    }
+    // pageable C: D2H into a pinned slot, copied out by the host threads one
+    // chunk behind (the slot of chunk ci - 2 was drained in iteration ci - 1)
+    float *hc = static_cast<float *>(mimw::pinned_slot(7 + (ci & 1), (size_t)achunk * n * 4));
+    require(hc != nullptr, MIMW_ERR_CUDA, "cudaHostAlloc failed");
+    check_cuda(cudaMemcpy2DAsync(hc, sizeof(float) * n, static_cast<char *>(dC.p) + (size_t)r0 * np * 4,
                                  sizeof(float) * np, sizeof(float) * n, rows, cudaMemcpyDeviceToHost, ds),
                "D2H c");
+    check_cuda(cudaEventRecord(e_d[ci].e, ds), "event");
+    if (ci >= 1) drain(ci - 1);
   }
+  if (c_pageable && nchunks > 0) drain(nchunks - 1);
   check_cuda(cudaStreamSynchronize(ds), "gemm execution");
   check_cuda(cudaStreamSynchronize(cs), "gemm execution");
   check_cuda(cudaStreamSynchronize(s), "gemm execution");
@@ -291,7 +355,15 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   const int nseg = precision == MIMW_PREC_F32_BF16X3 ? 3 : 1;
   static const int host_stage = getenv("MIMW_HOST_STAGE") ? atoi(getenv("MIMW_HOST_STAGE")) : 3;  // A/B knob (mode 3 9.9-10.0 ms vs device staging 11.2)
   if (nseg == 1 && host_stage) {
-    host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds, host_stage);
+    // pageable inputs: every chunk is rounded by the host threads (mode 1), so
+    // no cudaMemcpyAsync ever reads pageable memory (the driver would stage it
+    // synchronously at a fraction of the PCIe rate); pageable C: D2H through
+    // pinned slots
+    bool in_pageable = false;
+    for (size_t i = 0; i < a_parts.size(); ++i)
+      if (k_parts[i]) in_pageable |= !dma_capable(a_parts[i]) || !dma_capable(b_parts[i]);
+    host_gemm_host_staged(a_parts, b_parts, k_parts, m, n, k, c, s, cs, ds, in_pageable ? 1 : host_stage,
+                          !dma_capable(c));
     return;
   }
   const int64_t kp = round_up(k, 8);  // bf16 row pitch multiple of 16 B
@@ -301,6 +373,7 @@ void host_gemm(const std::vector<const float *> &a_parts, const std::vector<cons
   for (size_t i = 0; i < a_parts.size(); ++i) in_elems += (m + n) * k_parts[i];
   DevBuf din(sizeof(float) * in_elems, s);
   DevBuf dA(2 * m * kt, s), dB(2 * kt * np, s), dC(sizeof(float) * m * np, s);
+  UnwindSync guard(s, cs, ds);
   Event e_alloc, e_b;
   check_cuda(cudaEventRecord(e_alloc.e, s), "event");
   check_cuda(cudaStreamWaitEvent(cs, e_alloc.e, 0), "wait");
@@ -422,59 +495,121 @@ void host_attention_f32(const float *const *inputs, int n_inputs, float *o, floa
   check_cuda(cudaStreamSynchronize(s), "attention f32 execution");
 }
 
-// o[s,d] (+ lse[s]) = oracle_attention(q, k, v, w, scale) for one head of
-// host f32 Tiles (oracles.cpp:119-145).  Head dim is zero-padded to 128 (exact:
+// oracle_attention (oracles.cpp:119-145) for `heads` independent [seq, d]
+// heads of host f32 Tiles stored back to back ([heads, seq, d]); heads == 1
+// is exactly the reference signature.  Head dim zero-padded to 128 (exact:
 // padded q/k columns add 0 to every score, padded v columns give 0 outputs).
-void host_attention(const float *q, const float *k, const float *v, float *o, float *lse,
-                    int64_t seq, int64_t d, int64_t w, double scale, int precision = MIMW_PREC_BF16) {
+// Pipelined over chunks of heads on three streams, with the f32 <-> bf16
+// conversions on the host threads into pinned slots, so PCIe carries 2 bytes
+// per element in both directions and pageable caller buffers (the reference's
+// Tile is a std::vector, sim.hpp:13-26) are read and written by the host
+// threads at memory speed instead of through the driver's pageable staging:
+//   host: round chunk c -> slot   cs: H2D c   s: FA c   ds: D2H O_c (bf16), lse_c
+//   host: widen O_(c-1) -> o (exact)
+void host_attention_heads(const float *q, const float *k, const float *v, float *o, float *lse,
+                          int64_t heads, int64_t seq, int64_t d, int64_t w, double scale,
+                          int precision = MIMW_PREC_BF16) {
   require(precision == MIMW_PREC_BF16 || precision == MIMW_PREC_F32, MIMW_ERR_ARG,
           "precision must be MIMW_PREC_BF16 or MIMW_PREC_F32");
-  require(seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(heads >= 0 && seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
   require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
-  require(w >= 1 || seq == 0, MIMW_ERR_ARG, "window must be >= 1");
-  if (seq == 0 || d == 0) {
-    if (o && seq) std::memset(o, 0, sizeof(float) * seq * d);
-    if (lse && seq && d == 0)
-      for (int64_t i = 0; i < seq; ++i) lse[i] = std::log((float)std::min<int64_t>(w, i + 1));
+  require(w >= 1 || seq == 0 || heads == 0, MIMW_ERR_ARG, "window must be >= 1");
+  require(seq < (1ll << 31) && heads * ((seq + 255) / 256) < (1ll << 31), MIMW_ERR_UNSUPPORTED,
+          "extent too large");
+  if (heads == 0 || seq == 0) return;
+  if (d == 0) {
+    if (lse)
+      for (int64_t h = 0; h < heads; ++h)
+        for (int64_t i = 0; i < seq; ++i) lse[h * seq + i] = std::log((float)std::min<int64_t>(w, i + 1));
     return;
   }
   require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
   require_sm100();
   if (precision == MIMW_PREC_F32) {
-    const float *in[3] = {q, k, v};
-    host_attention_f32(in, 3, o, lse, seq, d, w, 1, false, scale);
+    for (int64_t h = 0; h < heads; ++h) {
+      const float *in[3] = {q + h * seq * d, k + h * seq * d, v + h * seq * d};
+      host_attention_f32(in, 3, o + h * seq * d, lse ? lse + h * seq : nullptr, seq, d, w, 1, false, scale);
+    }
     return;
   }
-  cudaStream_t s = cudaStreamPerThread;
-  const int64_t n = seq * d;
-  DevBuf din(sizeof(float) * 3 * n, s);
-  DevBuf dq(2 * seq * 128, s), dk(2 * seq * 128, s), dv(2 * seq * 128, s), dout(2 * seq * 128, s);
-  DevBuf dlse(sizeof(float) * seq, s), dof(sizeof(float) * n, s);
-  float *f = din.as<float>();
-  check_cuda(cudaMemcpyAsync(f, q, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D q");
-  check_cuda(cudaMemcpyAsync(f + n, k, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D k");
-  check_cuda(cudaMemcpyAsync(f + 2 * n, v, sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D v");
-  mimw::stage_cols_bf16(f, seq, d, 128, dq.p, 128, 0, 0, s);
-  mimw::stage_cols_bf16(f + n, seq, d, 128, dk.p, 128, 0, 0, s);
-  mimw::stage_cols_bf16(f + 2 * n, seq, d, 128, dv.p, 128, 0, 0, s);
-  check_cuda(cudaGetLastError(), "staging kernels");
-  mimw::AttnArgs a{};
-  a.q = dq.p;
-  a.k = dk.p;
-  a.v = dv.p;
-  a.o = dout.p;
-  a.lse = dlse.as<float>();
-  a.batch = 1;
-  a.heads = 1;
-  a.seq = seq;
-  a.window = w;
-  a.scale = scale;
-  check_cuda(mimw::attention_fwd_launch(a, s), "attention launch");
-  mimw::unpad_bf16_to_f32(dout.p, 128, dof.as<float>(), seq, d, s);
-  check_cuda(cudaGetLastError(), "unpad");
-  check_cuda(cudaMemcpyAsync(o, dof.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H o");
-  if (lse) check_cuda(cudaMemcpyAsync(lse, dlse.p, sizeof(float) * seq, cudaMemcpyDeviceToHost, s), "D2H lse");
+  cudaStream_t s = cudaStreamPerThread, cs = side_stream(0), ds = side_stream(1);
+  const int64_t he = seq * 128;  // padded elements per head and tensor
+  const int64_t ch = std::max<int64_t>(1, std::min<int64_t>(heads, (32ll << 20) / (3 * he * 2)));
+  const int64_t nchunks = (heads + ch - 1) / ch;
+  const size_t in_bytes = (size_t)3 * ch * he * 2, o_bytes = (size_t)ch * he * 2;
+  const size_t out_bytes = o_bytes + (size_t)ch * seq * 4;
+  DevBuf din(2 * in_bytes, s), dout(2 * out_bytes, s);
+  UnwindSync guard(s, cs, ds);
+  Event ev_alloc, ev_in[2], ev_fa[2], ev_out[2];
+  bool used[2] = {false, false};
+  check_cuda(cudaEventRecord(ev_alloc.e, s), "event");
+  check_cuda(cudaStreamWaitEvent(cs, ev_alloc.e, 0), "wait");
+  check_cuda(cudaStreamWaitEvent(ds, ev_alloc.e, 0), "wait");
+  auto widen = [&](int64_t c) {
+    const int b = (int)(c & 1);
+    const int64_t h0 = c * ch, nh = std::min(ch, heads - h0);
+    check_cuda(cudaEventSynchronize(ev_out[b].e), "attention execution");
+    const uint16_t *ho = static_cast<const uint16_t *>(mimw::pinned_slot(5 + b, out_bytes));
+    mimw::host_parallel_for(nh * seq, [&](int64_t lo, int64_t hi) {
+      mimw::host_rows_bf16_to_f32(ho + lo * 128, 128, hi - lo, d, o + (h0 * seq + lo) * d, d);
+    });
+    if (lse) std::memcpy(lse + h0 * seq, reinterpret_cast<const char *>(ho) + o_bytes, (size_t)nh * seq * 4);
+  };
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t h0 = c * ch, nh = std::min(ch, heads - h0);
+    if (used[b]) check_cuda(cudaEventSynchronize(ev_in[b].e), "pinned slot reuse");  // H2D of c-2 done
+    uint16_t *hin = static_cast<uint16_t *>(mimw::pinned_slot(3 + b, in_bytes));
+    uint16_t *hout = static_cast<uint16_t *>(mimw::pinned_slot(5 + b, out_bytes));
+    require(hin != nullptr && hout != nullptr, MIMW_ERR_CUDA, "cudaHostAlloc failed");
+    const float *src3[3] = {q, k, v};
+    mimw::host_parallel_for(3 * nh * seq, [&](int64_t lo, int64_t hi) {
+      for (int64_t r = lo; r < hi; ++r) {
+        const int64_t t = r / (nh * seq), rr = r - t * nh * seq;
+        uint16_t *dst = hin + t * ch * he + rr * 128;
+        mimw::host_rows_to_bf16(src3[t] + (h0 * seq + rr) * d, d, 1, d, dst, 128, 0);
+        if (d < 128) std::memset(dst + d, 0, (size_t)(128 - d) * 2);
+      }
+    });
+    uint16_t *dq = din.as<uint16_t>() + (size_t)b * 3 * ch * he;
+    if (used[b]) check_cuda(cudaStreamWaitEvent(cs, ev_fa[b].e, 0), "wait");  // FA of c-2 read its inputs
+    for (int t = 0; t < 3; ++t)
+      check_cuda(cudaMemcpyAsync(dq + t * ch * he, hin + t * ch * he, (size_t)nh * he * 2, cudaMemcpyHostToDevice, cs),
+                 "H2D q/k/v");
+    check_cuda(cudaEventRecord(ev_in[b].e, cs), "event");
+    check_cuda(cudaStreamWaitEvent(s, ev_in[b].e, 0), "wait");
+    char *dob = static_cast<char *>(dout.p) + (size_t)b * out_bytes;
+    if (used[b]) check_cuda(cudaStreamWaitEvent(s, ev_out[b].e, 0), "wait");  // D2H of c-2 read its outputs
+    mimw::AttnArgs a{};
+    a.q = dq;
+    a.k = dq + ch * he;
+    a.v = dq + 2 * ch * he;
+    a.o = dob;
+    a.lse = reinterpret_cast<float *>(dob + o_bytes);
+    a.batch = 1;
+    a.heads = nh;
+    a.seq = seq;
+    a.window = w;
+    a.scale = scale;
+    check_cuda(mimw::attention_fwd_launch(a, s), "attention launch");
+    check_cuda(cudaEventRecord(ev_fa[b].e, s), "event");
+    check_cuda(cudaStreamWaitEvent(ds, ev_fa[b].e, 0), "wait");
+    check_cuda(cudaMemcpyAsync(hout, dob, (size_t)nh * he * 2, cudaMemcpyDeviceToHost, ds), "D2H o");
+    if (lse)
+      check_cuda(cudaMemcpyAsync(reinterpret_cast<char *>(hout) + o_bytes, dob + o_bytes, (size_t)nh * seq * 4,
+                                 cudaMemcpyDeviceToHost, ds), "D2H lse");
+    check_cuda(cudaEventRecord(ev_out[b].e, ds), "event");
+    used[b] = true;
+    if (c >= 1) widen(c - 1);
+  }
+  widen(nchunks - 1);
+  check_cuda(cudaStreamSynchronize(cs), "attention execution");
   check_cuda(cudaStreamSynchronize(s), "attention execution");
+}
+
+void host_attention(const float *q, const float *k, const float *v, float *o, float *lse,
+                    int64_t seq, int64_t d, int64_t w, double scale, int precision = MIMW_PREC_BF16) {
+  host_attention_heads(q, k, v, o, lse, 1, seq, d, w, scale, precision);
 }
 
 void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *y, int64_t n_groups,
@@ -565,6 +700,51 @@ void host_simplicial(const float *q, const float *k1, const float *v1, const flo
   check_cuda(cudaStreamSynchronize(s), "simplicial execution");
 }
 
+// Argument checks shared by the public device GEMM entry and its tuning hook.
+// Returns false when there is nothing to launch (empty output, or K == 0,
+// for which C has been zero-filled: oracles.cpp:19).
+bool gemm_device_checks(const void *a, const void *b, void *c, int64_t m, int64_t n, int64_t k, int64_t lda,
+                        int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype, void *stream) {
+  require(b_layout == MIMW_B_KN || b_layout == MIMW_B_NK, MIMW_ERR_ARG, "bad b_layout");
+  require(c_dtype == MIMW_F32 || c_dtype == MIMW_BF16, MIMW_ERR_ARG, "bad c_dtype");
+  require(m >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
+  if (m == 0 || n == 0) return false;
+  const int64_t es = c_dtype == MIMW_F32 ? 4 : 2;
+  if (k == 0) {  // C = 0 (oracles.cpp:19)
+    require(c != nullptr, MIMW_ERR_ARG, "null pointer");
+    require(ldc >= n, MIMW_ERR_SHAPE, "leading dimension smaller than the row");
+    require_sm100();
+    check_cuda(cudaMemset2DAsync(c, ldc * es, 0, n * es, m, static_cast<cudaStream_t>(stream)), "memset");
+    return false;
+  }
+  require(a && b && c, MIMW_ERR_ARG, "null pointer");
+  require(lda >= k && ldc >= n && ldb >= (b_layout == MIMW_B_KN ? n : k), MIMW_ERR_SHAPE,
+          "leading dimension smaller than the row");
+  require_pitch(a, lda, 2, "a");
+  require_pitch(b, ldb, 2, "b");
+  require_pitch(c, ldc, es, "c");
+  require_sm100();
+  return true;
+}
+
+// Argument checks shared by the public device attention entry and its hook.
+bool attention_device_checks(const void *q, const void *k, const void *v, const void *o, int64_t batch,
+                             int64_t heads, int64_t seq, int64_t head_dim, int64_t window) {
+  require(batch >= 0 && heads >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
+  require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device attention supports head_dim == 128");
+  require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
+          "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
+  require(seq < (1ll << 31) && batch * heads * ((seq + 255) / 256) < (1ll << 31), MIMW_ERR_UNSUPPORTED,
+          "extent too large");
+  if (batch == 0 || heads == 0 || seq == 0) return false;
+  require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
+  require(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) % 16 == 0, MIMW_ERR_UNSUPPORTED,
+          "tensors must be 16-byte aligned");
+  require_sm100();
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -572,6 +752,13 @@ extern "C" {
 int mimw_b200_version(void) { return 1; }
 
 const char *mimw_b200_last_error(void) { return g_last_error.c_str(); }
+
+int mimw_b200_trim_pool(void) {
+  return guarded([&] {
+    cudaMemPool_t pool = mimw::scratch_pool();
+    if (pool) check_cuda(cudaMemPoolTrimTo(pool, 0), "cudaMemPoolTrimTo");
+  });
+}
 
 int mimw_b200_oracle_gemm(const float *a, const float *b, float *c, int64_t m, int64_t n, int64_t k,
                           int32_t precision) {
@@ -588,25 +775,7 @@ int mimw_b200_gemm_bf16(const void *a, const void *b, void *c, int64_t m, int64_
                         int64_t lda, int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype,
                         void *stream) {
   return guarded([&] {
-    require(b_layout == MIMW_B_KN || b_layout == MIMW_B_NK, MIMW_ERR_ARG, "bad b_layout");
-    require(c_dtype == MIMW_F32 || c_dtype == MIMW_BF16, MIMW_ERR_ARG, "bad c_dtype");
-    require(m >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
-    require(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
-    if (m == 0 || n == 0) return;
-    if (k == 0) {  // C = 0 (oracles.cpp:19)
-      require(c != nullptr, MIMW_ERR_ARG, "null pointer");
-      require_sm100();
-      const int64_t es = c_dtype == MIMW_F32 ? 4 : 2;
-      check_cuda(cudaMemset2DAsync(c, ldc * es, 0, n * es, m, static_cast<cudaStream_t>(stream)), "memset");
-      return;
-    }
-    require(a && b && c, MIMW_ERR_ARG, "null pointer");
-    require(lda >= k && ldc >= n && ldb >= (b_layout == MIMW_B_KN ? n : k), MIMW_ERR_SHAPE,
-            "leading dimension smaller than the row");
-    require_pitch(a, lda, 2, "a");
-    require_pitch(b, ldb, 2, "b");
-    require_pitch(c, ldc, c_dtype == MIMW_F32 ? 4 : 2, "c");
-    require_sm100();
+    if (!gemm_device_checks(a, b, c, m, n, k, lda, ldb, ldc, b_layout, c_dtype, stream)) return;
     mimw::GemmArgs g{};
     g.a = a;
     g.b = b;
@@ -634,20 +803,17 @@ int mimw_b200_oracle_attention_ex(const float *q, const float *k, const float *v
   return guarded([&] { host_attention(q, k, v, o, lse, seq, d, w, scale, precision); });
 }
 
+int mimw_b200_oracle_attention_heads(const float *q, const float *k, const float *v, float *o, float *lse,
+                                     int64_t heads, int64_t seq, int64_t d, int64_t w, double scale,
+                                     int32_t precision) {
+  return guarded([&] { host_attention_heads(q, k, v, o, lse, heads, seq, d, w, scale, precision); });
+}
+
 int mimw_b200_attention_fwd(const void *q, const void *k, const void *v, void *o, float *lse,
                             int64_t batch, int64_t heads, int64_t seq, int64_t head_dim,
                             int64_t window, double scale, void *stream) {
   return guarded([&] {
-    require(batch >= 0 && heads >= 0 && seq >= 0, MIMW_ERR_SHAPE, "negative extent");
-    require(head_dim == 128, MIMW_ERR_UNSUPPORTED, "device attention supports head_dim == 128");
-    require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
-            "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
-    require(seq < (1ll << 31) && batch * heads < (1ll << 31), MIMW_ERR_UNSUPPORTED, "extent >= 2^31");
-    if (batch == 0 || heads == 0 || seq == 0) return;
-    require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
-    require(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) % 16 == 0, MIMW_ERR_UNSUPPORTED,
-            "tensors must be 16-byte aligned");
-    require_sm100();
+    if (!attention_device_checks(q, k, v, o, batch, heads, seq, head_dim, window)) return;
     mimw::AttnArgs a{};
     a.q = q;
     a.k = k;
@@ -859,11 +1025,8 @@ int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void
                                double scale, int32_t emu, int32_t max_ctas, void *trace,
                                void *stream) {
   return guarded([&] {
-    if (batch == 0 || heads == 0 || seq == 0) return;
-    require(q && k && v && o, MIMW_ERR_ARG, "null pointer");
-    require(window >= 1 || window == MIMW_WINDOW_NONCAUSAL, MIMW_ERR_ARG,
-            "window must be >= 1 (or MIMW_WINDOW_NONCAUSAL)");
-    require_sm100();
+    if (!attention_device_checks(q, k, v, o, batch, heads, seq, 128, window)) return;
+    require(emu >= -1 && emu <= 4 && max_ctas >= 0, MIMW_ERR_ARG, "bad emu / max_ctas");
     mimw::AttnArgs a{};
     a.q = q;
     a.k = k;
@@ -891,19 +1054,8 @@ int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int
   return guarded([&] {
     require(cta_group == 1 || cta_group == 2 || cta_group == 4, MIMW_ERR_ARG,
             "cta_group must be 1, 2 or 4 (two CTA pairs sharing B by multicast)");
-    if (m == 0 || n == 0) return;
-    if (k == 0) {  // C = 0 (oracles.cpp:19)
-      require(c != nullptr, MIMW_ERR_ARG, "null pointer");
-      require_sm100();
-      const int64_t es = c_dtype == MIMW_F32 ? 4 : 2;
-      check_cuda(cudaMemset2DAsync(c, ldc * es, 0, n * es, m, static_cast<cudaStream_t>(stream)), "memset");
-      return;
-    }
-    require(a && b && c, MIMW_ERR_ARG, "null pointer");
-    require_pitch(a, lda, 2, "a");
-    require_pitch(b, ldb, 2, "b");
-    require_pitch(c, ldc, c_dtype == MIMW_F32 ? 4 : 2, "c");
-    require_sm100();
+    require(max_clusters >= 0, MIMW_ERR_ARG, "bad max_clusters");
+    if (!gemm_device_checks(a, b, c, m, n, k, lda, ldb, ldc, b_layout, c_dtype, stream)) return;
     mimw::GemmArgs g{};
     g.a = a;
     g.b = b;

@@ -853,6 +853,12 @@ cudaError_t multi_device_gemm_launch(const MultiDeviceGemmArgs &g, cudaStream_t 
   gs->rank = g.rank;
   gs->world = g.world;
   gs->epoch = g.epoch;
+  {
+    // MIMW_PEER_WAIT_S: seconds a rank waits for its peers at the device-side
+    // entry / exit barriers before trapping (default 600; 0 = wait forever)
+    static const double peer_s = getenv("MIMW_PEER_WAIT_S") ? atof(getenv("MIMW_PEER_WAIT_S")) : 600.0;
+    gs->peer_budget = peer_s > 0 ? (uint64_t)(peer_s * 2.1e9) : 0;
+  }
   gs->ctr = ctr;
   gs->max_slabs = L.max_slabs;
   gs->box = box;

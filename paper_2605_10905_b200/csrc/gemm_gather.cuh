@@ -43,6 +43,7 @@ struct GatherSched : SchedT<1> {
   uint32_t *pad_local;        // this rank's signal pad: IN[MAX_SPLITS], OUT[MAX_SPLITS]; null = no barrier
   uint32_t *pad_peer[MAX_SPLITS];
   uint32_t epoch;
+  uint64_t peer_budget;       // cycles a peer-dependent wait may spin before trapping (0 = forever)
   int rank, world;
   __device__ __forceinline__ int nslabs(int q) const { return (ks[q] + COMM_SLAB - 1) / COMM_SLAB; }
   // B boxes of slab j (K rows of the slab that exist, R at a time)
@@ -214,10 +215,10 @@ __device__ __forceinline__ void gather_entry(const GatherSched &sp, bool leader)
     for (int p = 0; p < sp.world; ++p)
       if (p != sp.rank) st_release_sys(sp.pad_peer[p] + sp.rank, sp.epoch);
     for (int p = 0; p < sp.world; ++p)
-      if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + p, sp.epoch, 20);
+      if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + p, sp.epoch, 20, sp.peer_budget);
     st_release_gpu(go, 1u);
   } else {
-    flag_wait_geq<false>(go, 1u, 21);
+    flag_wait_geq<false>(go, 1u, 21, sp.peer_budget);
   }
 }
 
@@ -234,7 +235,7 @@ __device__ __forceinline__ void gather_exit(const GatherSched &sp, bool leader, 
   for (int p = 0; p < sp.world; ++p)
     if (p != sp.rank) st_release_sys(sp.pad_peer[p] + MAX_SPLITS + sp.rank, sp.epoch);
   for (int p = 0; p < sp.world; ++p)
-    if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + MAX_SPLITS + p, sp.epoch, 24);
+    if (p != sp.rank) flag_wait_geq<true>(sp.pad_local + MAX_SPLITS + p, sp.epoch, 24, sp.peer_budget);
 }
 
 __device__ __forceinline__ void gather_agent_lag(const GatherSched &sp, uint32_t buf0, uint32_t bar0,

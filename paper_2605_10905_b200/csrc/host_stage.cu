@@ -146,6 +146,34 @@ void host_rows_to_bf16(const float *src, int64_t ld_src, int64_t rows, int64_t c
   if (avx2) _mm_sfence();  // streaming stores ordered before the caller hands the slot to the DMA
 }
 
+// bf16 -> f32 widening (exact) of device results staged into a pinned slot
+__attribute__((target("avx2"))) static void widen_row_avx2(const uint16_t *src, int64_t n, float *dst) {
+  int64_t j = 0;
+  for (; j + 8 <= n; j += 8) {
+    const __m256i w = _mm256_cvtepu16_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(src + j)));
+    _mm256_storeu_si256(reinterpret_cast<__m256i *>(dst + j), _mm256_slli_epi32(w, 16));
+  }
+  for (; j < n; ++j) {
+    const uint32_t u = (uint32_t)src[j] << 16;
+    std::memcpy(dst + j, &u, 4);
+  }
+}
+
+void host_rows_bf16_to_f32(const uint16_t *src, int64_t ld_src, int64_t rows, int64_t cols, float *dst,
+                           int64_t ld_dst) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  for (int64_t r = 0; r < rows; ++r) {
+    if (avx2) {
+      widen_row_avx2(src + r * ld_src, cols, dst + r * ld_dst);
+    } else {
+      for (int64_t j = 0; j < cols; ++j) {
+        const uint32_t u = (uint32_t)src[r * ld_src + j] << 16;
+        std::memcpy(dst + r * ld_dst + j, &u, 4);
+      }
+    }
+  }
+}
+
 namespace {
 // per calling thread: concurrent host entries (the reference's oracles are
 // pure functions, safe to call from several threads) never share a buffer

@@ -14,6 +14,10 @@ namespace mimw {
 void host_rows_to_bf16(const float *src, int64_t ld_src, int64_t rows, int64_t cols, uint16_t *dst,
                        int64_t ld_dst, int64_t col_off);
 
+// dst[r * ld_dst + j] = f32(src[r * ld_src + j]) for bf16 src (exact widening)
+void host_rows_bf16_to_f32(const uint16_t *src, int64_t ld_src, int64_t rows, int64_t cols, float *dst,
+                           int64_t ld_dst);
+
 // Runs f(lo, hi) over [0, n) split across the process-wide host thread pool
 // (the caller participates) and returns when every range is done.
 void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)> &f);

@@ -603,17 +603,21 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 __device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
 
-// Spin until *p >= target (acquire at gpu or sys scope); traps after the
-// watchdog budget like every mbarrier wait.
+// Spin until *p >= target (acquire at gpu or sys scope).  Traps after
+// `budget` cycles (default: the watchdog budget of every mbarrier wait);
+// budget 0 waits forever.  Waits that depend on a PEER device having launched
+// (the all-gather GEMM's entry / exit barriers) pass the much longer,
+// configurable peer budget (MIMW_PEER_WAIT_S), so a straggling rank is waited
+// for instead of killing every other rank's context.
 template <bool SYS>
-__device__ __forceinline__ void flag_wait_geq(const uint32_t *p, uint32_t target, int tag) {
+__device__ __forceinline__ void flag_wait_geq(const uint32_t *p, uint32_t target, int tag,
+                                              uint64_t budget = MIMW_WATCHDOG_CYCLES) {
   auto ld = [&] { return SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p); };
   if ((int32_t)(ld() - target) >= 0) return;
   const uint64_t t0 = clock64();
   while ((int32_t)(ld() - target) < 0) {
-    __nanosleep(32);
-    if (clock64() - t0 > MIMW_WATCHDOG_CYCLES)
-      watchdog_trap((uint32_t)(uintptr_t)p, target, tag);
+    __nanosleep(SYS ? 256 : 32);
+    if (budget && clock64() - t0 > budget) watchdog_trap((uint32_t)(uintptr_t)p, target, tag);
   }
 }
 

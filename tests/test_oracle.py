@@ -192,3 +192,113 @@ def test_attention_bwd_oracle_matches_torch_f64(causal, w):
         # the causal mode of the restatement is the reference's oracle_attention
         o_ref = oracle.oracle_attention(q, k, v, w if w is not None else s, scale)
         np.testing.assert_allclose(o_ref, O.detach().numpy(), rtol=1e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# config-scale checkers, pinned to the unmodified reference
+# ---------------------------------------------------------------------------
+@ref
+@pytest.mark.parametrize("r,k,n,threads", [(1, 1, 1, 1), (37, 300, 200, 3), (17, 1000, 1030, 8)])
+def test_gemm_rowlist_bit_exact_vs_reference(r, k, n, threads):
+    """The threaded k-outer restatement used by the config-scale tests gives
+    the reference's float sums bit for bit (oracles.cpp:17-23)."""
+    a = oracle.random_tile([r, k], 31 * r + k)
+    b = oracle.round_bf16(oracle.random_tile([k, n], 7 * n + 1))
+    want = np.empty((r, n), np.float32)
+    oracle.REF.ref_oracle_gemm(a, b, want, r, n, k)
+    got = oracle.oracle_gemm_rowlist(a, b, threads=threads)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_attention_rowlist_matches_rows():
+    q, k, v = (oracle.random_tile([300, 64], 40 + i) for i in range(3))
+    rows = [299, 0, 150, 7, 128]
+    o, lse = oracle.oracle_attention_rowlist(q, k, v, 100, 0.125, rows, threads=3)
+    for i, r in enumerate(rows):
+        want, wl = oracle.oracle_attention_rows(q, k, v, 100, 0.125, r, r + 1)
+        assert np.array_equal(o[i], want[0]) and lse[i] == wl[0]
+
+
+@ref
+@pytest.mark.parametrize("s,d,w1,w2", [(32, 16, 2, 16), (50, 8, 5, 50), (40, 12, 40, 3)])
+def test_simplicial_rows_vs_reference(s, d, w1, w2):
+    """oracle.oracle_simplicial_rows (the f64 numpy checker of every device
+    simplicial test) against the unmodified oracle_simplicial_attention
+    (oracles.cpp:82-117) through oracle/_ref: every row, o at 1e-5 (the
+    reference accumulates o in f32), lse at 1e-6."""
+    xs = [oracle.random_tile([s, d], oracle.input_seed(31 + s, i)) for i in range(5)]
+    want_o = np.empty((s, d), np.float32)
+    want_l = np.empty(s, np.float32)
+    oracle.REF.ref_oracle_simplicial_attention(*xs, want_o, want_l, s, d, w1, w2, 0.25)
+    got_o, got_l = oracle.oracle_simplicial_rows(*xs, w1, w2, 0.25, list(range(s)))
+    assert oracle.rel_error(got_o, want_o) <= 1e-5
+    assert oracle.rel_error_rows(got_o, want_o) <= 1e-5
+    np.testing.assert_allclose(got_l, want_l, rtol=1e-6, atol=1e-6)
+    # and the C restatement (the full-oracle checker) bit for bit in lse, f32-close in o
+    c_o, c_l = oracle.oracle_simplicial_attention(*xs, w1, w2, 0.25)
+    assert oracle.rel_error(c_o, want_o) <= 1e-6
+    assert np.array_equal(c_l, want_l)
+
+
+def _ref_attention(q, k, v, w, scale):
+    s, d = q.shape
+    out = np.empty((s, d), np.float32)
+    oracle.REF.ref_oracle_attention(np.ascontiguousarray(q, np.float32), np.ascontiguousarray(k, np.float32),
+                                    np.ascontiguousarray(v, np.float32), out, s, d, w, scale)
+    return out
+
+
+def _ref_noncausal(q, k, v, scale):
+    """Non-causal attention from the REFERENCE's causal oracle_attention by the
+    last-row trick: with w >= S, row S-1 attends every key, so putting query i
+    in the last row gives non-causal row i (oracles.cpp:123-126)."""
+    s, d = q.shape
+    out = np.empty((s, d), np.float32)
+    for i in range(s):
+        qi = q.copy()
+        qi[s - 1] = q[i]
+        out[i] = _ref_attention(qi, k, v, s, scale)[s - 1]
+    return out
+
+
+@ref
+@pytest.mark.parametrize("s,d", [(1, 8), (33, 16), (64, 32)])
+def test_noncausal_rows_pinned_to_reference(s, d):
+    """orc_attention_mode_rows(causal=0) (the checker of every non-causal
+    device test) equals the reference's own oracle row bit for bit."""
+    q, k, v = (oracle.random_tile([s, d], 500 + s + i) for i in range(3))
+    got, _ = oracle.oracle_attention_full(q, k, v, 0.3)
+    want = _ref_noncausal(q, k, v, 0.3)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@ref
+@pytest.mark.parametrize("causal,w", [(True, None), (True, 9), (False, None)])
+def test_attention_bwd_pinned_to_reference_finite_differences(causal, w):
+    """orc_attention_bwd (the f64 checker of the device backward) against
+    central differences of the REFERENCE's oracle_attention (through _ref; the
+    non-causal forward by the last-row trick): for L = <dO, O(q, k, v)>,
+    <dX, delta> ~= (L(X + eps delta) - L(X - eps delta)) / (2 eps) for random
+    directions delta in q, k and v."""
+    s, d, scale, eps = 24, 16, 0.3, 1e-2
+    rng = np.random.default_rng(17 + int(causal) + (w or 0))
+    q, k, v, do = (oracle.random_tile([s, d], 700 + i).astype(np.float64) for i in range(4))
+    ww = w if w is not None else s
+
+    def fwd(q_, k_, v_):
+        if causal:
+            return _ref_attention(q_, k_, v_, ww, scale).astype(np.float64)
+        return _ref_noncausal(q_.astype(np.float32), k_.astype(np.float32), v_.astype(np.float32),
+                              scale).astype(np.float64)
+
+    grads = oracle.oracle_attention_bwd(q, k, v, do, scale, causal=causal, w=w)
+    for which in range(3):
+        for _ in range(3):
+            delta = rng.standard_normal((s, d))
+            args_p = [q, k, v]
+            args_m = [q, k, v]
+            args_p = [x + eps * delta if i == which else x for i, x in enumerate(args_p)]
+            args_m = [x - eps * delta if i == which else x for i, x in enumerate(args_m)]
+            fd = (np.sum(do * fwd(*args_p)) - np.sum(do * fwd(*args_m))) / (2 * eps)
+            an = float(np.sum(grads[which].astype(np.float64) * delta))
+            assert abs(fd - an) <= 5e-4 * max(1.0, abs(an)), (which, fd, an)  # measured ~1e-5

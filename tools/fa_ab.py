@@ -1,13 +1,14 @@
-"""A/B timing of the FA forward between two builds of the library on one box:
-    python tools/fa_ab.py <lib_a.so> <lib_b.so> [rounds]"""
+"""A/B timing of the FA forward between builds of the library on one box:
+    python tools/fa_ab.py <lib_a.so> <lib_b.so> [<lib_c.so> ...] [rounds]"""
 import sys
 import os
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_10905_b200 as P  # noqa: E402
 
-libs = sys.argv[1:3]
-rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+libs = [a for a in sys.argv[1:] if a.endswith(".so")]
+rest = [a for a in sys.argv[1:] if not a.endswith(".so")]
+rounds = int(rest[0]) if rest else 3
 q, k, v = ((torch.rand((4, 32, 8192, 128), device="cuda") * 2 - 1).bfloat16() for _ in range(3))
 flop = 4.0 * 128 * 128 * 8192 * 8192 / 2
 handles = []
@@ -32,4 +33,4 @@ for r in range(rounds):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        print(r, os.path.basename(path), round(flop / ms / 1e9, 1), flush=True)
+        print(r, os.path.relpath(path), round(flop / ms / 1e9, 1), flush=True)

@@ -417,7 +417,8 @@ def bench_gemm(args, rank, ws, local):
         "data": "synthetic U[-1,1] bf16 (random init, no dataset)",
         "config": {"workload": "configs[1]: warp-specialized bf16 GEMM M=N=K=8192 (tiles by cluster launch control), "
                                "2-CTA clusters (cta_group::2), fp32 accumulate in TMEM, bf16 out",
-                   "M": GEMM_M, "N": GEMM_N, "K": GEMM_K, "tile": "256x256x64, 6-stage ring",
+                   "M": GEMM_M, "N": GEMM_N, "K": GEMM_K,
+                   "tile": "256x512x64 per CTA pair (gemm_wide.cuh), 4-stage ring, register-drained epilogue",
                    "parallelism": f"{ws} independent GEMM batches (one per GPU)",
                    "l2": "inputs 2 x 128 MiB > 126 MB L2 (no flush)"},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2),

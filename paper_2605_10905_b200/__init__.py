@@ -60,7 +60,7 @@ def lib() -> C.CDLL:
         L.mimw_b200_oracle_multi_device_gemm.argtypes = [_fp] * 5 + [_i64] * 4 + [C.c_int32]
         L.mimw_b200_gemm_bf16.argtypes = [_vp, _vp, _vp] + [_i64] * 6 + [C.c_int32, C.c_int32, _vp]
         L.mimw_b200_gemm_bf16_ex.argtypes = ([_vp, _vp, _vp] + [_i64] * 6 +
-                                             [C.c_int32] * 5 + [_vp])
+                                             [C.c_int32] * 6 + [_vp])
         for name, types in _optional_sigs().items():
             if hasattr(L, name):
                 getattr(L, name).argtypes = types
@@ -256,9 +256,10 @@ def _stream(stream):
 
 
 def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_group: int = 2,
-         raster_group: int = 0, max_clusters: int = 0):
+         raster_group: int = 0, max_clusters: int = 0, tile_n: int = 0):
     """C = A.B with bf16 A [M,K], B [K,N] (B_KN) or [N,K] (B_NK); fp32 accumulate.
-    ``out`` dtype float32 or bfloat16."""
+    ``out`` dtype float32 or bfloat16.  ``tile_n``: C columns per CTA-pair tile
+    (0 auto, 256, or 512 for bf16 out with cta_group 2)."""
     import torch
     _need(a, torch.bfloat16, "gemm a", 2)
     _need(b, torch.bfloat16, "gemm b", 2)
@@ -282,7 +283,7 @@ def gemm(a, b, out=None, b_layout: int = B_KN, out_dtype=None, stream=None, cta_
     cd = F32 if out.dtype == torch.float32 else BF16
     _check(lib().mimw_b200_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k,
                                         a.stride(0), b.stride(0), out.stride(0), b_layout, cd,
-                                        cta_group, raster_group, max_clusters, _stream(stream)))
+                                        cta_group, raster_group, max_clusters, tile_n, _stream(stream)))
     return out
 
 

@@ -25,6 +25,9 @@
 #include "attention_bwd.h"
 #include "attention_f32.h"
 #include "gemm_bf16.h"
+#ifdef MIMW_TILE_TRACE
+namespace mimw { cudaError_t set_tile_trace(void *buf); }
+#endif
 #include "gemm_mxfp8.h"
 #include "layernorm_cluster.h"
 #include "simplicial_fwd.h"
@@ -1045,15 +1048,24 @@ int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void
   });
 }
 
+#ifdef MIMW_TILE_TRACE
+// trace builds only (tools/moe_trace.py): per-tile timeline buffer, 4 u64 per tile
+int mimw_b200_debug_tile_trace(void *buf) {
+  return guarded([&] { check_cuda(mimw::set_tile_trace(buf), "tile trace"); });
+}
+#endif
+
 // Tuning / test hook (not part of the public header): force cta_group and
 // raster group.  Used by the parity tests to cover the 1-CTA variant.
 int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int64_t n, int64_t k,
                            int64_t lda, int64_t ldb, int64_t ldc, int32_t b_layout, int32_t c_dtype,
                            int32_t cta_group, int32_t raster_group, int32_t max_clusters,
-                           void *stream) {
+                           int32_t tile_n, void *stream) {
   return guarded([&] {
     require(cta_group == 1 || cta_group == 2 || cta_group == 4, MIMW_ERR_ARG,
             "cta_group must be 1, 2 or 4 (two CTA pairs sharing B by multicast)");
+    require(tile_n == 0 || tile_n == 256 || (tile_n == 512 && cta_group == 2 && c_dtype == MIMW_BF16),
+            MIMW_ERR_ARG, "tile_n must be 0 (auto), 256, or 512 (cta_group 2, bf16 out)");
     require(max_clusters >= 0, MIMW_ERR_ARG, "bad max_clusters");
     if (!gemm_device_checks(a, b, c, m, n, k, lda, ldb, ldc, b_layout, c_dtype, stream)) return;
     mimw::GemmArgs g{};
@@ -1072,6 +1084,7 @@ int mimw_b200_gemm_bf16_ex(const void *a, const void *b, void *c, int64_t m, int
     g.cluster_pairs = cta_group == 4 ? 2 : 1;
     g.raster_group = raster_group;
     g.max_clusters = max_clusters;
+    g.tile_n = tile_n;
     check_cuda(mimw::gemm_bf16_launch(g, static_cast<cudaStream_t>(stream)), "gemm launch");
   });
 }

@@ -38,6 +38,21 @@
 
 namespace mimw {
 
+#ifdef MIMW_TILE_TRACE
+// Per-tile timeline (tools/moe_trace.py; trace builds only): tile t ->
+// {MMA start, last MMA issued, accumulator seen by the epilogue, smid}, ns.
+__device__ unsigned long long *g_mimw_tile_trace;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TILE_TRACE(t, slot, v) \
+  do { if (g_mimw_tile_trace) g_mimw_tile_trace[(size_t)(t) * 4 + (slot)] = (v); } while (0)
+#else
+#define TILE_TRACE(t, slot, v) do {} while (0)
+#endif
+
 namespace {
 
 constexpr int BK = 64;           // K per stage (one 128-byte swizzle row of bf16)
@@ -132,6 +147,7 @@ struct GroupedSched {
   int n_chunks, num_n, bm;         // bm = rows per cluster tile (128 * CG)
   int swap;                        // tail tiles (< bm rows) use swapped operands (CG == 2)
   int clc;                         // tiles dispatched by cluster launch control (grid = one cluster per tile)
+  int prefetch;                    // W k-blocks prefetched into L2 ahead of the TMA loads (0 = off)
   __device__ __forceinline__ int num_tiles() const { return chunk_off[n_chunks]; }
   __device__ __forceinline__ TileCoord decode(int t) const {
     int lo = 0, hi = n_chunks - 1;  // last chunk with chunk_off[c] <= t
@@ -332,6 +348,22 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const uint32_t sb = sa + C::A_BYTES;
           const int k0 = kb * BK;
           if constexpr (GROUPED) {
+            // Weight panels stream from DRAM once per group, and each CTA keeps
+            // only ~96 KiB of them in flight, so the loads run at the
+            // latency-bound per-SM rate (tools/moe_trace.py).  Warm L2 `prefetch`
+            // k-blocks ahead of the ring instead.
+            if (sched.prefetch > 0) {
+              const int k_lo = kb == 0 ? 0 : kb + sched.prefetch - 1;
+              const int k_hi = min(num_k - 1, kb + sched.prefetch - 1);
+              for (int kp = k_lo; kp <= k_hi; ++kp) {
+                if constexpr (B_MN) {
+#pragma unroll
+                  for (int j = 0; j < C::NB_CTA / 64; ++j) tma_prefetch_l2_3d(&tmB, n0 + j * 64, kp * BK, tc.e);
+                } else {
+                  tma_prefetch_l2_3d(&tmB, kp * BK, n0, tc.e);
+                }
+              }
+            }
             // W[e] through the 3-D map: (n, k, e) for [G,K,N], (k, n, e) for [G,N,K]
             if constexpr (CG == 2) tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
             else tma_load_2d(sa, &tmA, fb, k0, m0);
@@ -395,6 +427,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const uint32_t idesc = swap_n ? idesc_bf16(BM_CTA * CG, swap_n, B_MN ? 1 : 0, 0) : C::IDESC;
         mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1, 2);
         tc_fence_after();
+        if (lane_id() == 0) TILE_TRACE(t, 0, gtimer());
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(full_bar(stage), phase, 3);
@@ -427,6 +460,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        if (lane_id() == 0) TILE_TRACE(t, 1, gtimer());
         if (++acc == ACC_STAGES) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -468,6 +502,14 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // Transpose 32 x 32 chunks through the staging buffer (SWIZZLE_64B).
         mbar_wait(tfull_bar(acc), acc_phase, 4);
         tc_fence_after();
+#ifdef MIMW_TILE_TRACE
+        if (warp == 2 && leader && lane == 0) {
+          uint32_t smid;
+          asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+          TILE_TRACE(t, 2, gtimer());
+          TILE_TRACE(t, 3, smid);
+        }
+#endif
         const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
         const int feat0 = tc.nt * BN + (int)rank * BM_CTA + q * 32;
         const int nch = tc.swap_n / EPI_COLS;
@@ -509,6 +551,14 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       mbar_wait(tfull_bar(acc), acc_phase, 4);
       tc_fence_after();
+#ifdef MIMW_TILE_TRACE
+      if (warp == 2 && leader && lane == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        TILE_TRACE(t, 2, gtimer());
+        TILE_TRACE(t, 3, smid);
+      }
+#endif
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int ch = 0; ch < BN / EPI_COLS; ++ch) {
@@ -633,6 +683,8 @@ CUtensorMap make_c_map(const void *c, int64_t rows, int64_t n, int64_t ldc) {
                       sizeof(OutT) == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+#include "gemm_wide.cuh"
+
 template <int CG, bool B_MN, typename OutT>
 cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
   using C = Cfg<CG, B_MN, OutT>;
@@ -648,6 +700,15 @@ cudaError_t launch_impl(const GemmArgs &g, cudaStream_t stream) {
   const int group = g.raster_group > 0 ? g.raster_group : 8;
   static const int clc_env = getenv("MIMW_GEMM_CLC_DENSE") ? atoi(getenv("MIMW_GEMM_CLC_DENSE")) : 1;  // A/B knob (CLC measured +0.4%)
   const int clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;
+  if constexpr (CG == 2 && sizeof(OutT) == 2) {
+    // 256 x 512 pair tiles (gemm_wide.cuh) when asked for, or by default when
+    // the problem still fills >= 3 waves of CTA pairs with them
+    static const int wide_env = getenv("MIMW_GEMM_WIDE") ? atoi(getenv("MIMW_GEMM_WIDE")) : 1;  // A/B knob
+    const int64_t wide_tiles = ((g.m + 255) / 256) * ((g.n + WIDE_BN - 1) / WIDE_BN);
+    const bool wide = g.cluster_pairs != 2 &&
+                      (g.tile_n == WIDE_BN || (g.tile_n == 0 && wide_env != 0 && wide_tiles >= 3 * (sm_count() / 2)));
+    if (wide) return launch_wide<B_MN>(g, stream, clc);
+  }
   if constexpr (CG == 2) {
     if (g.cluster_pairs == 2) {
       SchedT<2> s;
@@ -720,6 +781,8 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
     gs->bm = BM_CTA * CG;
     gs->swap = (CG == 2 && g.swap_tails) ? 1 : 0;
     gs->clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;  // max_clusters bounds a persistent grid
+    static const int pf_env = getenv("MIMW_MOE_PREFETCH") ? atoi(getenv("MIMW_MOE_PREFETCH")) : 0;  // A/B knob (16: 3.58 vs 3.47 ms, not kept)
+    gs->prefetch = pf_env;
     int first_live = -1;
     std::vector<int> live;
     for (int i = 0; i < cnt; ++i) {
@@ -791,6 +854,13 @@ GatherLayout gather_layout(int rank, int world, const int64_t *k, int64_t rows, 
   return L;
 }
 }  // namespace
+
+#ifdef MIMW_TILE_TRACE
+cudaError_t set_tile_trace(void *buf) {
+  unsigned long long *p = static_cast<unsigned long long *>(buf);
+  return cudaMemcpyToSymbol(g_mimw_tile_trace, &p, sizeof(p));
+}
+#endif
 
 cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream) {
   if (g.k == 0) {

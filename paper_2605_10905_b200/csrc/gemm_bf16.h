@@ -16,6 +16,7 @@ struct GemmArgs {
   int raster_group;  // tile-row group for L2-friendly rasterisation (0 = default 8)
   int max_clusters;  // 0 = one cluster per SM pair
   int cluster_pairs; // 2: clusters of two CTA pairs sharing B by TMA multicast; else 1
+  int tile_n;        // C columns per CTA-pair tile: 0 auto, 256, or 512 (bf16 out, cta_group 2)
 };
 
 cudaError_t gemm_bf16_launch(const GemmArgs &g, cudaStream_t stream);

@@ -107,6 +107,28 @@ def test_device_gemm_ragged(P, m, k, n, cta_group):
     assert oracle.rel_error(got, want) <= 1e-5
 
 
+@pytest.mark.parametrize("b_layout", ["kn", "nk"])
+@pytest.mark.parametrize("m,k,n", [(1024, 1024, 1024), (1, 8, 8), (130, 72, 264), (300, 136, 1000),
+                                   (257, 4104, 600), (513, 64, 1544), (2048, 192, 2056)])
+def test_device_gemm_wide_tiles(P, b_layout, m, k, n):
+    """256 x 512 pair tiles (gemm_wide.cuh): vs the oracle at the bf16 budget,
+    and bit-identical to the 256 x 256 kernel (same fp32 K order per element)."""
+    import torch
+    a, b, ta, tb = _dev_case(m, k, n, 3 * m + n + k)
+    want = oracle.oracle_gemm(a, b)
+    bl = P.B_KN if b_layout == "kn" else P.B_NK
+    tbb = tb if b_layout == "kn" else tb.t().contiguous()
+    guard = torch.full((m + 1, n), 3.0, device="cuda", dtype=torch.bfloat16)  # row m: must stay untouched
+    wide = P.gemm(ta, tbb, b_layout=bl, tile_n=512, out=guard[:m])
+    narrow = P.gemm(ta, tbb, b_layout=bl, tile_n=256)
+    torch.cuda.synchronize()
+    got = wide.float().cpu().numpy()
+    assert oracle.rel_error(got, want) <= BF16_TOL
+    assert oracle.rel_error_rows(got, want) <= BF16_TOL
+    assert torch.equal(wide, narrow)
+    assert torch.all(guard[m] == 3.0)
+
+
 def test_device_gemm_8192_sampled_rows(P):
     """configs[1] size: 8192^3 bf16, row-sampled exact oracle."""
     import torch

@@ -16,7 +16,7 @@ for what in "$@"; do
         > "$OUT/launches_bench.log" 2>&1 ;;
     gemm)
       timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
-        -k regex:"gemm_bf16_kernel.*SchedT<.int.1>" -s 3 -c 1 -o "$OUT/gemm" -f \
+        -k regex:"gemm_wide_kernel|gemm_bf16_kernel.*SchedT<.int.1>" -s 3 -c 1 -o "$OUT/gemm" -f \
         python bench.py --workload gemm --no-secondary --steps 2 --warmup 3 --no-e2e --no-cpu \
         > "$OUT/gemm_ncu.log" 2>&1 ;;
     fa)

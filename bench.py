@@ -464,7 +464,7 @@ def bench_attention(args, rank, ws, local):
     def step():
         P._check(L.mimw_b200_attention_fwd_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                               lse.data_ptr(), my, 1, FA_S, FA_S, scale, args.fa_emu,
-                                              0, None, sptr))
+                                              0, None, 1, sptr))
 
     steps = args.steps
     clk = Clocks(local)

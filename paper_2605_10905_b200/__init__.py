@@ -80,7 +80,7 @@ def _optional_sigs():
         "mimw_b200_attention_fwd": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_bwd": [_vp] * 5 + [_vp] + [_vp] * 3 + [_i64] * 5 + [C.c_double, _vp],
         "mimw_b200_attention_fwd_ex": [_vp, _vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_double, C.c_int32,
-                                                                           C.c_int32, _vp, _vp],
+                                                                           C.c_int32, _vp, C.c_int32, _vp],
         "mimw_b200_gemm_mxfp8": [_vp] * 5 + [_i64] * 3 + [_vp],
         "mimw_b200_oracle_simplicial_attention": [_fp] * 7 + [_i64] * 4 + [C.c_double],
         "mimw_b200_simplicial_attention_fwd": [_vp] * 6 + [_vp] + [_i64] * 5 + [C.c_double, _vp],
@@ -292,7 +292,7 @@ WINDOW_NONCAUSAL = 0
 
 def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None, out=None,
                   lse=None, want_lse: bool = True, stream=None, emu: int = -1, max_ctas: int = 0,
-                  trace=None, causal: bool = True):
+                  trace=None, causal: bool = True, cta_group: int = 1):
     """Causal (optionally windowed) or, with ``causal=False``, non-causal
     attention forward on bf16 [B, H, S, 128] CUDA tensors.  Returns (o, lse)
     with lse fp32 [B, H, S] (natural log)."""
@@ -326,7 +326,7 @@ def attention_fwd(q, k, v, window: int | None = None, scale: float | None = None
                                             lse.data_ptr() if lse is not None else None, b, h, s,
                                             window, scale, emu, max_ctas,
                                             trace.data_ptr() if trace is not None else None,
-                                            _stream(stream)))
+                                            cta_group, _stream(stream)))
     return out, lse
 
 

@@ -69,6 +69,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 #define MMA_WAIT mbar_wait
 #endif
 constexpr int kDefaultEmu = 0;  // exp2 pairs (of 8) evaluated on the FMA pipe (0: measured fastest, tools/fa_sweep.py)
+constexpr int kDefaultEmuCg2 = 2;  // same, 2-CTA kernel
 constexpr int HEAD_BAND = 4;    // heads per scheduling band (K/V of a band stays in L2)
 
 struct Params {
@@ -600,6 +601,45 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   }
 }
 
+#include "attention_fwd_cg2.cuh"
+
+template <int EMU>
+cudaError_t launch_cg2(const AttnArgs &a, const Params &p, cudaStream_t stream) {
+  const uint64_t bh = (uint64_t)a.batch * a.heads;
+  CUtensorMap tQ = make_tmap_3d(a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                (uint64_t)a.seq * D, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tK = make_tmap_3d(a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                (uint64_t)a.seq * D, 64, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tV = make_tmap_3d(a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tO = make_tmap_3d(a.o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
+                                (uint64_t)a.seq * D, 64, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  auto kern = attention_fwd_cg2_kernel<EMU>;
+#ifdef MIMW_FA_EVENTS
+  constexpr int smem_total = C2_SMEM_TOTAL + 12 * 128 * 8;  // + the event log
+#else
+  constexpr int smem_total = C2_SMEM_TOTAL;
+#endif
+  static_assert(smem_total <= 232448, "FA smem");
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
+  if (e != cudaSuccess) return e;
+  const int items = p.bh * p.nqb;
+  if (items == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * items, 1, 1);  // one cluster per work item; CLC hands them out
+  cfg.blockDim = dim3(C2_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem_total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tQ, tK, tV, tO, p);
+}
+
 constexpr int kCounterSlots = 1024;
 
 int *fa_counter_slot() {
@@ -645,6 +685,18 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   static const int dbg = getenv("MIMW_FA_DEBUG") ? atoi(getenv("MIMW_FA_DEBUG")) : 0;
   p.dbg = dbg;
   p.scale_pos = a.scale > 0 ? 1 : 0;
+  // 2-CTA kernel (attention_fwd_cg2.cuh) when asked for (measured slower
+  // than the one-CTA kernel on configs[3]: DESIGN.md §4.1)
+  static const int cg2_env = getenv("MIMW_FA_CG2") ? atoi(getenv("MIMW_FA_CG2")) : 0;  // A/B knob
+  if ((a.cta_group == 2 || cg2_env != 0) && a.max_ctas <= 0) {
+    switch (a.emu < 0 ? kDefaultEmuCg2 : a.emu) {
+      case 0: return launch_cg2<0>(a, p, stream);
+      case 1: return launch_cg2<1>(a, p, stream);
+      case 2: return launch_cg2<2>(a, p, stream);
+      case 3: return launch_cg2<3>(a, p, stream);
+      default: return launch_cg2<4>(a, p, stream);
+    }
+  }
   const int items = p.bh * p.nqb;
   int grid = sm_count();
   if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;

@@ -15,6 +15,7 @@ struct AttnArgs {
   int max_ctas;           // 0 = one persistent CTA per SM
   unsigned long long *trace = nullptr;  // optional [grid][12 warps][8] cycle counters
   int emu = -1;           // exp2 pairs of 8 on the FMA pipe (-1 = default)
+  int cta_group = 1;      // 1: one-CTA kernel (two Q tiles per SM); 2: the 2-CTA kernel (attention_fwd_cg2.cuh)
 };
 
 cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream);

@@ -1026,10 +1026,11 @@ int mimw_b200_grouped_gemm_bf16_ex(const void *x, const int64_t *m_offsets, cons
 int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void *o, float *lse,
                                int64_t batch, int64_t heads, int64_t seq, int64_t window,
                                double scale, int32_t emu, int32_t max_ctas, void *trace,
-                               void *stream) {
+                               int32_t cta_group, void *stream) {
   return guarded([&] {
     if (!attention_device_checks(q, k, v, o, batch, heads, seq, 128, window)) return;
     require(emu >= -1 && emu <= 4 && max_ctas >= 0, MIMW_ERR_ARG, "bad emu / max_ctas");
+    require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
     mimw::AttnArgs a{};
     a.q = q;
     a.k = k;
@@ -1044,6 +1045,7 @@ int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void
     a.emu = emu;
     a.max_ctas = max_ctas;
     a.trace = static_cast<unsigned long long *>(trace);
+    a.cta_group = cta_group;
     check_cuda(mimw::attention_fwd_launch(a, static_cast<cudaStream_t>(stream)), "attention launch");
   });
 }

@@ -212,7 +212,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader);
+      if (lane == 0) mbar_arrive_remote(tempty_leader);
       if (row0 >= sched.M) continue;
       // store: 32-column chunks through a swizzled 2 KiB box (SWIZZLE_64B:
       // 16-B chunk c of row r at c ^ ((r >> 1) & 3)) and a TMA store

@@ -76,6 +76,34 @@ def test_device_attention_vs_oracle(P, b, h, s, window):
         assert np.max(np.abs(lse[head] - wlse)) <= 1e-3 * max(1.0, np.max(np.abs(wlse)))
 
 
+@pytest.mark.parametrize("b,h,s,window,amp,causal", [(1, 2, 1000, 1000, 1.0, True), (1, 2, 777, 129, 1.0, True),
+                                                      (2, 2, 513, 64, 1.0, True), (1, 2, 1024, 1024, 8.0, True),
+                                                      (1, 1, 640, 640, 8.0, False)])
+def test_device_attention_2cta_vs_oracle(P, b, h, s, window, amp, causal):
+    """The 2-CTA kernel (attention_fwd_cg2.cuh, cta_group=2): same oracle
+    bar; amp 8 scales the scores so the running max moves and O is rescaled
+    (the cross-warpgroup hand-off and the PV(j-1) wait of that path)."""
+    import torch
+    xs, ts = _bf16_heads(b, h, s, 128, 7 * s + window)
+    ramp = torch.linspace(0.1, 3.0, s, device="cuda")[None, None, :, None] * amp
+    ts[0] = (ts[0].float() * ramp).bfloat16()
+    xs[0] = ts[0].float().cpu().numpy().reshape(b * h, s, 128)
+    scale = 128 ** -0.5
+    o, lse = P.attention_fwd(*ts, window=window, scale=scale, causal=causal, cta_group=2)
+    torch.cuda.synchronize()
+    o = o.float().cpu().numpy().reshape(b * h, s, 128)
+    lse = lse.cpu().numpy().reshape(b * h, s)
+    for head in range(b * h):
+        if causal:
+            want, wlse = oracle.oracle_attention(xs[0][head], xs[1][head], xs[2][head], window, scale,
+                                                 with_lse=True)
+        else:
+            want, wlse = oracle.oracle_attention_full(xs[0][head], xs[1][head], xs[2][head], scale)
+        assert oracle.rel_error(o[head], want) <= TOL, head
+        assert oracle.rel_error_rows(o[head], want) <= 2 * TOL, head
+        assert np.max(np.abs(lse[head] - wlse)) <= 1e-3 * max(1.0, np.max(np.abs(wlse)))
+
+
 def test_device_attention_full_config_sampled(P):
     """configs[3] size B=4 H=32 S=8192 D=128 causal: row-sampled exact oracle
     on a few (b, h) heads + whole-tensor properties."""

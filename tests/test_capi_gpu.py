@@ -122,7 +122,7 @@ def test_wrapper_validation(P):
     # the C hooks check alignment / extents too
     L = P.lib()
     base = q.data_ptr()
-    r = L.mimw_b200_attention_fwd_ex(base + 2, base, base, base, None, 1, 1, 256, 256, 0.1, -1, 0, None, None)
+    r = L.mimw_b200_attention_fwd_ex(base + 2, base, base, base, None, 1, 1, 256, 256, 0.1, -1, 0, None, 1, None)
     assert r == P.ERR_UNSUPPORTED and b"aligned" in L.mimw_b200_last_error()
     r = L.mimw_b200_gemm_bf16_ex(a.data_ptr(), a.data_ptr(), a.data_ptr(), 64, 64, 128, 100, 64, 64, 0, 1, 2, 0,
                                  0, 0, None)

@@ -675,6 +675,16 @@ def bench_moe(args, rank, ws, local):
     per_launch = secs / steps
     achieved = flop_mine / per_launch / 1e12
     bytes_mine = 2.0 * (per * MOE_K * MOE_N + int(offs[-1]) * (MOE_K + MOE_N))
+    # same-box library reference: torch._grouped_mm (CUTLASS grouped GEMM in
+    # PyTorch) on the same operands and steps, for context only
+    lib_ref = None
+    try:
+        offs_dev = torch.from_numpy(offs[1:].astype(np.int32)).to(dev)
+        lsecs = timed(lambda: torch._grouped_mm(x[:int(offs[-1])], w[:per], offs=offs_dev), steps, args.warmup,
+                      ws, stream)
+        lib_ref = round(flop_mine * steps / lsecs / 1e12, 2)
+    except Exception as e:  # noqa: BLE001
+        lib_ref = f"unavailable: {type(e).__name__}"
     reasm = None
     if ws > 1:
         full_offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
@@ -700,7 +710,8 @@ def bench_moe(args, rank, ws, local):
                          "hbm_gbs_min_bytes": round(bytes_mine / per_launch / 1e9, 1),
                          "hbm_peak_gbs": pk["hbm"],
                          "traffic": traffic("grouped_moe") if ws == 1 else None,
-                         "algorithmic_flop_per_launch": flop_mine},
+                         "algorithmic_flop_per_launch": flop_mine,
+                         "torch_grouped_mm_tflops_same_box": lib_ref},
             "gpu_launches": steps, "clocks": clocks}
 
 

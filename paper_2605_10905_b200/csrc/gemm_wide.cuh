@@ -154,6 +154,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, lane_id() == 0)) {
         mbar_wait_cluster(tempty_bar, acc_phase ^ 1, 2);
         tc_fence_after();
+        if (lane_id() == 0) TILE_TRACE(t, 0, gtimer());
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(full_bar(stage), phase, 3);
           tc_fence_after();
@@ -178,6 +179,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           __syncwarp();
           if (++stage == WIDE_STAGES) { stage = 0; phase ^= 1; }
         }
+        if (lane_id() == 0) TILE_TRACE(t, 1, gtimer());
         acc_phase ^= 1;
       }
     }
@@ -198,6 +200,9 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(tfull_bar, acc_phase, 4);
       acc_phase ^= 1;
       tc_fence_after();
+#ifdef MIMW_TILE_TRACE
+      if (warp == 2 && leader && lane == 0) TILE_TRACE(t, 2, gtimer());
+#endif
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * 256;
       // drain 256 fp32 columns into 128 packed-bf16 registers, then release TMEM
       uint32_t pk[128];
@@ -213,6 +218,9 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(tempty_leader);
+#ifdef MIMW_TILE_TRACE
+      if (warp == 2 && leader && lane == 0) TILE_TRACE(t, 3, gtimer());
+#endif
       if (row0 >= sched.M) continue;
       // store: 32-column chunks through a swizzled 2 KiB box (SWIZZLE_64B:
       // 16-B chunk c of row r at c ^ ((r >> 1) & 3)) and a TMA store

@@ -90,7 +90,7 @@ def _optional_sigs():
         "mimw_b200_gemm_mxfp8_ex": [_vp] * 5 + [_i64] * 3 + [C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32, _vp],
         "mimw_b200_grouped_gemm_bf16_ex": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, C.c_int32,
-                                           C.c_int32, C.c_int32, C.c_int32, _vp],
+                                           C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp],
     }
 
 
@@ -344,11 +344,13 @@ def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None, cta_group: int = 2):
 
 
 def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, cta_group: int = 2,
-                 max_clusters: int = 0, swap_tails: bool = True):
+                 max_clusters: int = 0, swap_tails: bool | None = None, tile_n: int = 0):
     """Grouped (MoE) GEMM: for each group e, ``out[off[e]:off[e+1]] =
     x[off[e]:off[e+1]] @ W_e`` with bf16 x [rows, K], w [G, K, N] (B_KN) or
     [G, N, K] (B_NK) CUDA tensors and ``m_offsets`` a host sequence of G+1
-    non-decreasing row offsets.  Returns bf16 [rows, N]."""
+    non-decreasing row offsets.  Returns bf16 [rows, N].  ``tile_n``: output
+    columns per CTA-pair tile (0 auto, 256, 512); ``swap_tails``: groups'
+    < 256-row tails as swapped-operand tiles (None: the tile's default)."""
     import torch
     offs = np.ascontiguousarray(np.asarray(m_offsets, dtype=np.int64))
     g = w.shape[0]
@@ -366,8 +368,8 @@ def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, c
         out = torch.empty((x.shape[0], n), device=x.device, dtype=torch.bfloat16)
     _check(lib().mimw_b200_grouped_gemm_bf16_ex(x.data_ptr(), offs.ctypes.data, w.data_ptr(),
                                                 out.data_ptr(), g, n, k, w_layout, cta_group,
-                                                max_clusters, 1 if swap_tails else 0,
-                                                _stream(stream)))
+                                                max_clusters, -1 if swap_tails is None else int(bool(swap_tails)),
+                                                tile_n, _stream(stream)))
     return out
 
 

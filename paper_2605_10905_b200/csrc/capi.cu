@@ -617,9 +617,11 @@ void host_attention(const float *q, const float *k, const float *v, float *o, fl
 
 void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *y, int64_t n_groups,
                   int64_t n, int64_t k, int32_t w_layout, int cta_group, int max_clusters,
-                  bool swap_tails, cudaStream_t stream) {
+                  int swap_tails, int tile_n, cudaStream_t stream) {
   require(w_layout == MIMW_B_KN || w_layout == MIMW_B_NK, MIMW_ERR_ARG, "bad w_layout");
   require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
+  require(tile_n == 0 || tile_n == 256 || (tile_n == 512 && cta_group == 2), MIMW_ERR_ARG,
+          "tile_n must be 0 (auto), 256, or 512 (cta_group 2)");
   require(n_groups >= 0 && n >= 0 && k >= 0, MIMW_ERR_SHAPE, "negative extent");
   if (n_groups == 0 || n == 0) return;
   require(m_offsets != nullptr, MIMW_ERR_ARG, "null m_offsets");
@@ -647,6 +649,7 @@ void grouped_gemm(const void *x, const int64_t *m_offsets, const void *w, void *
   g.cta_group = cta_group;
   g.max_clusters = max_clusters;
   g.swap_tails = swap_tails;
+  g.tile_n = tile_n;
   check_cuda(mimw::grouped_gemm_bf16_launch(g, stream), "grouped gemm launch");
 }
 
@@ -924,7 +927,7 @@ int mimw_b200_grouped_gemm_bf16(const void *x, const int64_t *m_offsets, const v
                                 int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
                                 void *stream) {
   return guarded([&] {
-    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, true,
+    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, 2, 0, -1, 0,
                  static_cast<cudaStream_t>(stream));
   });
 }
@@ -1014,10 +1017,11 @@ int mimw_b200_oracle_layernorm(const float *x, const float *w, const float *b, d
 int mimw_b200_grouped_gemm_bf16_ex(const void *x, const int64_t *m_offsets, const void *w, void *y,
                                    int64_t n_groups, int64_t n, int64_t k, int32_t w_layout,
                                    int32_t cta_group, int32_t max_clusters, int32_t swap_tails,
-                                   void *stream) {
+                                   int32_t tile_n, void *stream) {
   return guarded([&] {
-    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, cta_group, max_clusters,
-                 swap_tails != 0, static_cast<cudaStream_t>(stream));
+    require(swap_tails >= -1 && swap_tails <= 1, MIMW_ERR_ARG, "swap_tails must be -1, 0 or 1");
+    grouped_gemm(x, m_offsets, w, y, n_groups, n, k, w_layout, cta_group, max_clusters, swap_tails, tile_n,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 

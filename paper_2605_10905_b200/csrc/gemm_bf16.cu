@@ -756,6 +756,53 @@ std::vector<int> grouped_order(const std::vector<int> &live, const int *rows, in
   return out;
 }
 
+// Grouped GEMM on the 256 x 512 wide tile (gemm_wide.cuh, padded tails):
+// one launch per <= MAX_GROUPS groups.
+template <bool B_MN>
+cudaError_t grouped_wide_impl(const GroupedGemmArgs &g, cudaStream_t stream, int clc) {
+  const int64_t total_rows = g.m_offsets[g.n_groups];
+  CUtensorMap tA = make_tmap_2d(g.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, total_rows, g.k, g.k, BK, BM_CTA,
+                                CU_TENSOR_MAP_SWIZZLE_128B);
+  auto *gs = new GroupedWideSched;
+  cudaError_t err = cudaSuccess;
+  for (int64_t g0 = 0; g0 < g.n_groups && err == cudaSuccess; g0 += MAX_GROUPS) {
+    const int cnt = (int)std::min<int64_t>(MAX_GROUPS, g.n_groups - g0);
+    const char *wbase = static_cast<const char *>(g.w) + (size_t)g0 * g.k * g.n * 2;
+    CUtensorMap tB = B_MN ? make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.n, g.k, cnt, g.n,
+                                         g.k * g.n, 64, BK, 1, CU_TENSOR_MAP_SWIZZLE_128B)
+                          : make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, cnt, g.k,
+                                         g.k * g.n, BK, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    std::memset(gs, 0, sizeof(GroupedWideSched));
+    gs->n_groups = cnt;
+    gs->num_n = (int)((g.n + WIDE_BN - 1) / WIDE_BN);
+    gs->clc = clc;
+    // default swapped: configs[4] in 50-launch blocks 3.66 ms vs 3.96 padded vs 3.80 (256 x 256 tiles);
+    // padded is faster only from a cold start (3.20 vs 3.33 ms), where it does 20% more MMA work
+    gs->swap = g.swap_tails != 0 ? 1 : 0;
+    int first_live = -1, tiles = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t r0 = g.m_offsets[g0 + i], r1 = g.m_offsets[g0 + i + 1];
+      gs->row_off[i] = (int)r0;
+      gs->rows[i] = (int)(r1 - r0);
+      gs->mt[i] = (int)((r1 - r0 + 255) / 256);
+      gs->tile_pref[i] = tiles;
+      tiles += gs->mt[i] * gs->num_n;
+      if (r1 > r0) {
+        gs->y[i] = make_c_map<__nv_bfloat16>(static_cast<char *>(g.y) + (size_t)r0 * g.n * 2, r1 - r0, g.n, g.n);
+        if (first_live < 0) first_live = i;
+      }
+    }
+    gs->tile_pref[cnt] = tiles;
+    if (first_live < 0) continue;
+    for (int i = 0; i < cnt; ++i)
+      if (gs->rows[i] == 0) gs->y[i] = gs->y[first_live];  // never stored through
+    err = launch_wide_kernel<B_MN>(tA, tB, gs->y[first_live], (int)g.n, (int)g.k, *gs, tiles, g.max_clusters, clc,
+                                   stream);
+  }
+  delete gs;
+  return err;
+}
+
 // One launch per chunk of <= MAX_GROUPS groups (the Y maps travel in the
 // kernel's parameter block).
 template <int CG, bool B_MN>
@@ -779,7 +826,7 @@ cudaError_t grouped_impl(const GroupedGemmArgs &g, cudaStream_t stream) {
     std::memset(gs, 0, sizeof(GroupedSched));
     gs->num_n = (int)((g.n + BN - 1) / BN);
     gs->bm = BM_CTA * CG;
-    gs->swap = (CG == 2 && g.swap_tails) ? 1 : 0;
+    gs->swap = (CG == 2 && g.swap_tails != 0) ? 1 : 0;
     gs->clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;  // max_clusters bounds a persistent grid
     static const int pf_env = getenv("MIMW_MOE_PREFETCH") ? atoi(getenv("MIMW_MOE_PREFETCH")) : 0;  // A/B knob (16: 3.58 vs 3.47 ms, not kept)
     gs->prefetch = pf_env;
@@ -888,6 +935,13 @@ cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stre
   }
   if (g.cta_group == 1)
     return g.w_kn ? grouped_impl<1, true>(g, stream) : grouped_impl<1, false>(g, stream);
+  // 256 x 512 pair tiles (gemm_wide.cuh): configs[4] 3.20 vs 3.45 ms with 256 x 256
+  static const int wide_env = getenv("MIMW_MOE_WIDE") ? atoi(getenv("MIMW_MOE_WIDE")) : 1;  // A/B knob
+  static const int clc_env = getenv("MIMW_GEMM_CLC") ? atoi(getenv("MIMW_GEMM_CLC")) : 1;
+  if (g.tile_n == WIDE_BN || (g.tile_n == 0 && wide_env != 0 && g.n >= WIDE_BN)) {
+    const int clc = (clc_env != 0 && g.max_clusters <= 0) ? 1 : 0;
+    return g.w_kn ? grouped_wide_impl<true>(g, stream, clc) : grouped_wide_impl<false>(g, stream, clc);
+  }
   return g.w_kn ? grouped_impl<2, true>(g, stream) : grouped_impl<2, false>(g, stream);
 }
 

@@ -34,7 +34,9 @@ struct GroupedGemmArgs {
   bool w_kn;
   int cta_group;
   int max_clusters;
-  bool swap_tails;  // each group's < 256-row tail as a swapped-operand tile (Y^T = W^T X^T)
+  int swap_tails;   // each group's < 256-row tail as a swapped-operand tile (Y^T = W^T X^T):
+                    // 1 yes, 0 padded, -1 default (swapped)
+  int tile_n;       // output columns per CTA-pair tile: 0 auto (512 when n >= 512), 256, 512
 };
 
 cudaError_t grouped_gemm_bf16_launch(const GroupedGemmArgs &g, cudaStream_t stream);

@@ -38,10 +38,50 @@ constexpr int WIDE_BAR_BYTES = 256;
 constexpr int WIDE_SMEM = WIDE_BAR_OFF + WIDE_BAR_BYTES + 1024;  // + align slack
 static_assert(WIDE_SMEM <= 232448, "wide GEMM smem");
 
-template <bool B_MN>
+// Grouped (MoE) problems on the wide tile: every group's rows are cut into
+// 256-row M-tiles; N-tiles outer, M-tiles inner per group, so the pairs on
+// one weight panel run together and share it in L2.  A group's last tile of
+// t < 256 rows is computed with swapped operands (Y^T = W^T X^T: the
+// pair's two M = 256 MMAs run over the tile's 512 weight columns and N = t
+// rounded to 32 tokens), so its cost follows the weight panel it streams,
+// not a padded 256-row tile (swap = 0: padded; rows past m_e are clipped by
+// the group's Y map).  Measured at configs[4] (tools/moe_ab.py, 50-launch
+// blocks): 3.66 ms swapped, 3.96 padded, 3.80 with 256 x 256 tiles.
+struct GroupedWideSched {
+  static constexpr bool kGrouped = true;
+  CUtensorMap y[MAX_GROUPS];
+  int tile_pref[MAX_GROUPS + 1];  // prefix over groups of m_tiles * num_n
+  int mt[MAX_GROUPS];             // 256-row tiles of group e
+  int row_off[MAX_GROUPS];
+  int rows[MAX_GROUPS];
+  int n_groups, num_n, clc;
+  int swap;  // a group's < 256-row tail (and a group of < 256 rows) as a swapped-operand tile
+  __device__ __forceinline__ int num_tiles() const { return tile_pref[n_groups]; }
+  __device__ __forceinline__ TileCoord decode(int t) const {
+    int a = 0, b = n_groups - 1;  // last group with tile_pref[g] <= t (empty groups have no tiles)
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (tile_pref[mid] <= t) a = mid; else b = mid - 1;
+    }
+    const int r = t - tile_pref[a];
+    TileCoord c;
+    c.e = a;
+    c.mt = r % mt[a];
+    c.nt = r / mt[a];
+    c.row_base = row_off[a];
+    c.rows = rows[a];
+    const int tail = rows[a] - (mt[a] - 1) * 256;
+    c.swap_n = (swap && c.mt == mt[a] - 1 && tail < 256) ? ((tail + 31) & ~31) : 0;
+    return c;
+  }
+  __device__ __forceinline__ const CUtensorMap *c_map(const CUtensorMap *, int e) const { return &y[e]; }
+};
+
+template <bool B_MN, typename Prob>
 __global__ void __launch_bounds__(WIDE_THREADS, 1)
 gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmC, int N, int K, const Sched sched) {
+                 const __grid_constant__ CUtensorMap tmC, int N, int K, const __grid_constant__ Prob sched) {
+  constexpr bool GROUPED = Prob::kGrouped;
   constexpr uint32_t IDESC = idesc_bf16(256, 256, 0, B_MN ? 1 : 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -122,7 +162,9 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, true)) {
         if (clc) clc_request(u);
         const TileCoord tc = sched.decode(t);
-        const int m0 = tc.mt * 256 + (int)rank * BM_CTA;
+        // swapped tail: this CTA stages tokens [swap_n/2 * rank, +swap_n/2) of the tail as the
+        // MMAs' B operand (same 128-row box; the rows past it are not read by the MMA)
+        const int m0 = tc.row_base + tc.mt * 256 + (int)rank * (tc.swap_n ? tc.swap_n / 2 : BM_CTA);
         const int n0 = tc.nt * WIDE_BN + (int)rank * 128;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
@@ -134,7 +176,15 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            if constexpr (B_MN) {
+            if constexpr (GROUPED) {  // W[e] through the 3-D map: (n, k, e) for [G,K,N], (k, n, e) for [G,N,K]
+              if constexpr (B_MN) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                  tma_load_3d_cg2(sb + (2 * h + j) * (64 * BK * 2), &tmB, fb, n0 + h * 256 + j * 64, k0, tc.e);
+              } else {
+                tma_load_3d_cg2(sb + h * (128 * BK * 2), &tmB, fb, k0, n0 + h * 256, tc.e);
+              }
+            } else if constexpr (B_MN) {
 #pragma unroll
               for (int j = 0; j < 2; ++j)
                 tma_load_2d_cg2(sb + (2 * h + j) * (64 * BK * 2), &tmB, fb, n0 + h * 256 + j * 64, k0);
@@ -152,6 +202,10 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = cluster, u = 0; t < num_tiles; t = next_tile(t, u++, lane_id() == 0)) {
+        int swap_n = 0;
+        if constexpr (GROUPED) swap_n = sched.decode(t).swap_n;
+        // swapped: A = W^T (the B slot; MN-major for [G,K,N]), B = the tail's X rows (the A slot)
+        const uint32_t idesc = swap_n ? idesc_bf16(256, swap_n, B_MN ? 1 : 0, 0) : IDESC;
         mbar_wait_cluster(tempty_bar, acc_phase ^ 1, 2);
         tc_fence_after();
         if (lane_id() == 0) TILE_TRACE(t, 0, gtimer());
@@ -170,7 +224,8 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const uint64_t bdesc = B_MN ? smem_desc_sw128(sb + h * (128 * BK * 2), 64 * BK * 2, 1024)
                                             : smem_desc_sw128(sb + h * (128 * BK * 2), 16, 1024);
                 const uint64_t b_k = bdesc + (uint64_t)(B_MN ? ((k * UMMA_K * 128) >> 4) : ((k * UMMA_K * 2) >> 4));
-                mma_f16_ss<2>(tmem_base + h * 256, a_k, b_k, IDESC, (kb | k) != 0);
+                if (GROUPED && swap_n) mma_f16_ss<2>(tmem_base + h * 256, b_k, a_k, idesc, (kb | k) != 0);
+                else mma_f16_ss<2>(tmem_base + h * 256, a_k, b_k, idesc, (kb | k) != 0);
               }
             }
             mma_commit_cg2_mc(empty_bar(stage), 0x3);
@@ -204,16 +259,20 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (warp == 2 && leader && lane == 0) TILE_TRACE(t, 2, gtimer());
 #endif
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * 256;
-      // drain 256 fp32 columns into 128 packed-bf16 registers, then release TMEM
+      // drain 256 fp32 columns (swapped: swap_n token columns) into 128
+      // packed-bf16 registers, then release TMEM
+      const int ncols = tc.swap_n ? tc.swap_n : 256;
       uint32_t pk[128];
 #pragma unroll
       for (int ch = 0; ch < 16; ++ch) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(t_row + ch * 16, v);
-        tmem_ld_wait();
+        if (ch * 16 < ncols) {
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(t_row + ch * 16, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          pk[ch * 8 + e] = pack_bf16(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+          for (int e = 0; e < 8; ++e)
+            pk[ch * 8 + e] = pack_bf16(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -221,7 +280,39 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #ifdef MIMW_TILE_TRACE
       if (warp == 2 && leader && lane == 0) TILE_TRACE(t, 3, gtimer());
 #endif
-      if (row0 >= sched.M) continue;
+      const CUtensorMap *cmap = sched.c_map(&tmC, tc.e);
+      if (GROUPED && tc.swap_n) {
+        // swapped: TMEM lane = output feature, column = token.  Transpose 32
+        // tokens x 32 features per box through smem (SWIZZLE_64B) into Y rows.
+        const int feat0 = col0 + (int)rank * BM_CTA + q * 32;
+        if (feat0 >= N) continue;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const int tok0 = tc.mt * 256 + ch * 32;
+          if (ch * 32 < tc.swap_n && tok0 < tc.rows) {
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            const uint32_t sbuf = stage_base + buf * WIDE_EPI_BUF;
+            const uint32_t cbyte = (lane & 7) * 2;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const uint32_t pc = (lane >> 3) ^ ((r >> 1) & 3);
+              const uint32_t w = pk[ch * 16 + (r >> 1)];
+              const uint16_t hv = (r & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xFFFF);
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(sbuf + r * 64 + pc * 16 + cbyte), "h"(hv) : "memory");
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(cmap, sbuf, feat0, tok0);
+              bulk_commit();
+            }
+            buf ^= 1;
+          }
+        }
+        continue;
+      }
+      if (row0 >= tc.rows) continue;
       // store: 32-column chunks through a swizzled 2 KiB box (SWIZZLE_64B:
       // 16-B chunk c of row r at c ^ ((r >> 1) & 3)) and a TMA store
 #pragma unroll
@@ -240,7 +331,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, sbuf, col0 + ch * EPI_COLS, row0);
+            tma_store_2d(cmap, sbuf, col0 + ch * EPI_COLS, row0);
             bulk_commit();
           }
           buf ^= 1;
@@ -259,6 +350,30 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
+template <bool B_MN, typename Prob>
+cudaError_t launch_wide_kernel(const CUtensorMap &tA, const CUtensorMap &tB, const CUtensorMap &tC, int n, int k,
+                               const Prob &s, int tiles, int max_clusters, int clc, cudaStream_t stream) {
+  auto kern = gemm_wide_kernel<B_MN, Prob>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WIDE_SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(WIDE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = WIDE_SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = clc ? tiles : std::min(tiles, sm_count() / 2);
+  if (!clc && max_clusters > 0) clusters = std::min(clusters, max_clusters);
+  if (clusters <= 0) return cudaSuccess;
+  cfg.gridDim = dim3(clusters * 2, 1, 1);
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, n, k, s);
+}
+
 template <bool B_MN>
 cudaError_t launch_wide(const GemmArgs &g, cudaStream_t stream, int clc) {
   CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.k, g.lda, BK, BM_CTA,
@@ -275,23 +390,5 @@ cudaError_t launch_wide(const GemmArgs &g, cudaStream_t stream, int clc) {
   s.M = (int)g.m;
   s.clc = clc;
   const int tiles = s.num_m * s.num_n;
-  auto kern = gemm_wide_kernel<B_MN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WIDE_SMEM);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(WIDE_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = WIDE_SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int clusters = clc ? tiles : std::min(tiles, sm_count() / 2);
-  if (!clc && g.max_clusters > 0) clusters = std::min(clusters, g.max_clusters);
-  if (clusters <= 0) return cudaSuccess;
-  cfg.gridDim = dim3(clusters * 2, 1, 1);
-  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, (int)g.n, (int)g.k, s);
+  return launch_wide_kernel<B_MN>(tA, tB, tC, (int)g.n, (int)g.k, s, tiles, g.max_clusters, clc, stream);
 }

@@ -37,18 +37,20 @@ def _case(rows, k, n, seed, start=0, extra=0):
     return offs, x, w, tx, tw
 
 
-@pytest.mark.parametrize("cta_group,swap", [(1, False), (2, False), (2, True)])
+@pytest.mark.parametrize("cta_group,swap,tile_n", [(1, False, 0), (2, False, 256), (2, True, 256), (2, False, 512),
+                                                   (2, True, 512)])
 @pytest.mark.parametrize("w_layout", ["kn", "nk"])
-def test_grouped_ragged_full_oracle(P, cta_group, swap, w_layout):
+def test_grouped_ragged_full_oracle(P, cta_group, swap, tile_n, w_layout):
     """Ragged groups incl. empty, 1-row, exact-tile and tail-tile experts;
-    K and N not multiples of the tile; rows outside every group untouched."""
+    K and N not multiples of the tile; rows outside every group untouched.
+    tile_n 512: the 256 x 512 wide kernel, tails padded or swapped."""
     import torch
     rows = [0, 1, 130, 256, 0, 300, 77, 511, 33, 255, 128, 129, 96]
     offs, x, w, tx, tw = _case(rows, 264, 328, 11, start=5, extra=9)
     tww = tw if w_layout == "kn" else tw.transpose(1, 2).contiguous()
     out = torch.full((x.shape[0], 328), 3.0, device="cuda", dtype=torch.bfloat16)
     P.grouped_gemm(tx, offs, tww, out=out, w_layout=P.B_KN if w_layout == "kn" else P.B_NK,
-                   cta_group=cta_group, swap_tails=swap)
+                   cta_group=cta_group, swap_tails=swap, tile_n=tile_n)
     torch.cuda.synchronize()
     got = out.float().cpu().numpy()
     want = oracle.oracle_grouped_gemm(x, offs, w)

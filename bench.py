@@ -87,6 +87,13 @@ class Clocks:
             return
         self.th = threading.Thread(target=self._read, daemon=True)
         self.th.start()
+        # nvidia-smi needs a few hundred ms to emit its first sample: wait for
+        # it, then keep only the samples taken from here on (the timed region
+        # of a ~100-ms workload would otherwise see none)
+        t_end = time.time() + 3.0
+        while not self.rows and time.time() < t_end:
+            time.sleep(0.01)
+        self.rows.clear()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -210,6 +217,17 @@ def e2e_h2d_bytes(m, n, k):
         f32 = mode == 2 or (mode == 3 and i % 2 == 1)
         total += 4 * rows * k if f32 else 2 * rows * kp
     return total
+
+
+COOLDOWN_S = 2.0
+
+
+def cooldown(ws):
+    """Idle COOLDOWN_S seconds (all ranks) between the line's workloads."""
+    import torch
+    torch.cuda.synchronize()
+    time.sleep(COOLDOWN_S)
+    barrier(ws)
 
 
 def timed(step, steps, warmup, ws, stream):
@@ -1040,20 +1058,32 @@ def main():
     else:
         res = bench_gemm(args, rank, ws, local)
         if not args.no_secondary:
+            # each further workload starts after COOLDOWN_S idle seconds, so it
+            # is not measured in the power / clock state the previous one left
+            # behind (1 kW cap; e.g. LayerNorm read 3.9 instead of 5.4 TB/s
+            # right after the MoE line)
+            res["cooldown_s_between_workloads"] = COOLDOWN_S
+            cooldown(ws)
             fa = bench_attention(args, rank, ws, local)
             torch_empty_cache()
+            cooldown(ws)
             res["secondary"] = {"mxfp8_gemm": bench_mxfp8(args, rank, ws, local)}
             torch_empty_cache()
+            cooldown(ws)
             moe = bench_moe(args, rank, ws, local)
             res["secondary"]["grouped_moe_gemm"] = {k: moe[k] for k in (
                 "value", "unit", "ms_per_step", "scaling", "config", "roofline", "clocks",
                 "reassembly")}
             torch_empty_cache()
+            cooldown(ws)
             res["secondary"]["layernorm_cluster"] = bench_layernorm(args, rank, ws, local)
+            cooldown(ws)
             res["secondary"]["simplicial_attention"] = bench_simplicial(args, rank, ws, local)
             torch_empty_cache()
+            cooldown(ws)
             res["secondary"]["attention_bwd"] = bench_attention_bwd(args, rank, ws, local)
             torch_empty_cache()
+            cooldown(ws)
             try:
                 if ws > 1 and os.environ.get("MIMW_BENCH_MD", "1") == "0":
                     raise RuntimeError("disabled by MIMW_BENCH_MD=0")

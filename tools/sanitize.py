@@ -16,14 +16,21 @@ a = torch.randn(300, 200, device="cuda").bfloat16()
 b = torch.randn(200, 264, device="cuda").bfloat16()
 for cg in (1, 2, 4):
     P.gemm(a, b, cta_group=cg)
+bw = torch.randn(200, 1040, device="cuda").bfloat16()
+P.gemm(a, bw, tile_n=512)  # 256 x 512 wide tiles (register-drained epilogue)
+P.gemm(a, bw.t().contiguous(), b_layout=P.B_NK, tile_n=512)
 q, k, v = (torch.randn(1, 2, 300, 128, device="cuda").bfloat16() for _ in range(3))
 P.attention_fwd(q, k, v)
 P.attention_fwd(q, k, v, window=77)
+P.attention_fwd(q, k, v, window=77, cta_group=2)  # 2-CTA kernel
 offs = np.array([0, 5, 5, 300, 400], np.int64)
 x = torch.randn(400, 128, device="cuda").bfloat16()
 w = torch.randn(4, 128, 264, device="cuda").bfloat16()
 P.grouped_gemm(x, offs, w)
 P.grouped_gemm(x, offs, w, swap_tails=False)
+ww = torch.randn(4, 128, 1040, device="cuda").bfloat16()
+P.grouped_gemm(x, offs, ww, tile_n=512)  # wide, swapped tails
+P.grouped_gemm(x, offs, ww, tile_n=512, swap_tails=False)  # wide, padded tails
 qa = torch.randint(0, 120, (256, 256), device="cuda", dtype=torch.uint8)
 sa = torch.randint(120, 130, (256, 8), device="cuda", dtype=torch.uint8)
 for cg in (1, 2):

@@ -149,7 +149,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     tma_prefetch_desc(&tmV);
     for (int h = 0; h < 2; ++h) {
       mbar_init(q_full(h), 1);
-      mbar_init(q_empty(h), 4);
+      mbar_init(q_empty(h), 1);
       mbar_init(s_full(h), 1);
       mbar_init(p_full(h), 4);
       mbar_init(o_done(h), 1);
@@ -261,7 +261,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       MMA_WAIT(kv_full(pos % NSLOT), (pos / NSLOT) & 1, 23);
       MIMW_TR_END(2)
     };
-    auto issue_S = [&](int h, uint32_t kslot) {
+    auto issue_S = [&](int h, uint32_t kslot, bool last) {
       {
         MIMW_TR_BEGIN
         MMA_WAIT(s_free, sf_phase ^ 1, 24);  // S buffer released by its last reader
@@ -280,6 +280,9 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                         make_desc(LO_KMAJ | (kb + off), HI_KMAJ), IDESC_S, k != 0);
         }
         mma_commit(s_full(h));
+        // Q_h's last reader: release it when this MMA completes (not when the
+        // softmax has loaded S), so the next item's Q load starts earlier
+        if (last) mma_commit(q_empty(h));
       }
       __syncwarp();
       EV(21 + 2 * h);
@@ -341,8 +344,8 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         const uint32_t kpos = ring + 2 * (j - lo);
         if (s_role) {
           ring_wait(kpos);
-          if (j >= lo0 && j <= hi0) issue_S(0, kpos % NSLOT);
-          if (has1 && j >= lo1 && j <= hi1) issue_S(1, kpos % NSLOT);
+          if (j >= lo0 && j <= hi0) issue_S(0, kpos % NSLOT, j == hi0);
+          if (has1 && j >= lo1 && j <= hi1) issue_S(1, kpos % NSLOT, j == hi1);
           release(kpos % NSLOT);  // K_j: both S products issued
         } else {
           const uint32_t vpos = kpos + 1;  // V_j
@@ -427,13 +430,10 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         }
         tmem_ld_wait();
         EV(11);
-        // S is in registers: hand the buffer back (and Q_h after its last S)
+        // S is in registers: hand the buffer back
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(s_free);
-          if (j == hi) mbar_arrive(q_empty(h));
-        }
+        if (lane == 0) mbar_arrive(s_free);
         EV(12);
 #ifdef MIMW_FA_TRACE
         const long long tr2 = clock64();

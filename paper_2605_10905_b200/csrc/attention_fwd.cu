@@ -30,9 +30,10 @@
 // keeping the tensor pipe busy while both softmax warpgroups compute.
 // Correction (O *= 2^(m_old - m_new), only when the running max grows by
 // > 8 in log2 units) runs in the softmax warpgroup after PV_h(j-1) completes
-// and before P_h(j) is published.  The epilogue (O / l, lse) writes HBM
-// straight from registers, so the next Q tile can be loaded as soon as the
-// last S of the current one has been read.
+// and before P_h(j) is published.  The epilogue (O / l, lse) goes through a
+// per-warp 4 KiB swizzled smem box and TMA stores.  Q_h is released by a
+// tcgen05.commit after its last S MMA, so the next item's Q load overlaps the
+// current item's tail.
 #include "attention_fwd.h"
 #include "ptx.cuh"
 #include "softmax.cuh"

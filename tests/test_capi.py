@@ -93,3 +93,20 @@ def test_oracle_grouped_gemm_is_per_group_oracle_gemm():
     ys = oracle.oracle_grouped_gemm(x, offs, w)
     assert ys[1].shape == (0, 24)
     np.testing.assert_array_equal(ys[2], oracle.oracle_gemm(x[3:8], w[2]))
+
+
+def test_tile_and_variant_selectors_are_validated(L):
+    """The tuning hooks reject tile / variant selectors they do not implement
+    before touching any device state (no GPU needed): dense and grouped
+    tile_n, grouped swap_tails, attention cta_group."""
+    import paper_2605_10905_b200 as P
+    nul = None
+    offs = np.array([0, 4], np.int64)
+    r = L.mimw_b200_gemm_bf16_ex(nul, nul, nul, 64, 64, 64, 64, 64, 64, 0, 1, 2, 0, 0, 384, nul)
+    assert r == P.ERR_ARG and b"tile_n" in L.mimw_b200_last_error()
+    r = L.mimw_b200_gemm_bf16_ex(nul, nul, nul, 64, 64, 64, 64, 64, 64, 0, 0, 2, 0, 0, 512, nul)  # f32 out
+    assert r == P.ERR_ARG
+    r = L.mimw_b200_grouped_gemm_bf16_ex(nul, offs.ctypes.data, nul, nul, 1, 512, 64, 0, 1, 0, -1, 512, nul)
+    assert r == P.ERR_ARG and b"tile_n" in L.mimw_b200_last_error()  # 512-wide needs cta_group 2
+    r = L.mimw_b200_grouped_gemm_bf16_ex(nul, offs.ctypes.data, nul, nul, 1, 512, 64, 0, 2, 0, 2, 0, nul)
+    assert r == P.ERR_ARG and b"swap_tails" in L.mimw_b200_last_error()

@@ -56,6 +56,30 @@ def test_gemm_fuzz(P, m, n, k, pad_a, pad_b, b_nk, cg, seed):
 
 
 @SETTINGS
+@given(m=st.integers(1, 700), n=st.integers(1, 160).map(lambda x: 8 * x), k=st.integers(1, 80).map(lambda x: 8 * x),
+       pad_a=st.integers(0, 3).map(lambda x: 8 * x), pad_c=st.integers(0, 3).map(lambda x: 8 * x),
+       b_nk=st.booleans(), seed=st.integers(0, 10_000))
+def test_gemm_wide_fuzz(P, m, n, k, pad_a, pad_c, b_nk, seed):
+    """256 x 512 wide tiles (bf16 out, strided A and C views): bit-identical to
+    the 256 x 256 kernel and within the bf16 budget of the oracle."""
+    import torch
+    a = _bf16((m, k), seed)
+    b = _bf16((k, n), seed + 1)
+    ta = torch.zeros((m, k + pad_a), device="cuda", dtype=torch.bfloat16)
+    ta[:, :k] = torch.from_numpy(a).cuda().bfloat16()
+    tb = torch.from_numpy(np.ascontiguousarray(b.T) if b_nk else b).cuda().bfloat16()
+    bl = P.B_NK if b_nk else P.B_KN
+    cw = torch.full((m, n + pad_c), 7.0, device="cuda", dtype=torch.bfloat16)
+    P.gemm(ta[:, :k], tb, b_layout=bl, out=cw[:, :n], tile_n=512)
+    cn = P.gemm(ta[:, :k], tb, b_layout=bl, tile_n=256)
+    torch.cuda.synchronize()
+    assert torch.equal(cw[:, :n], cn)
+    assert torch.all(cw[:, n:] == 7.0)  # padding columns untouched
+    want = oracle.oracle_gemm(a, b)
+    assert oracle.rel_error(cn.float().cpu().numpy(), want) <= TOL
+
+
+@SETTINGS
 @given(s=st.integers(1, 700), bh=st.integers(1, 3), causal=st.booleans(),
        w=st.integers(1, 800), seed=st.integers(0, 10_000))
 def test_attention_fuzz(P, s, bh, causal, w, seed):
@@ -113,16 +137,20 @@ def test_simplicial_fuzz(P, s, bh, w1, w2, seed):
 
 @SETTINGS
 @given(sizes=st.lists(st.integers(0, 300), min_size=1, max_size=6), n=st.integers(1, 40).map(lambda x: 8 * x),
-       k=st.integers(1, 40).map(lambda x: 8 * x), nk=st.booleans(), cg=st.sampled_from([1, 2]),
+       k=st.integers(1, 40).map(lambda x: 8 * x), nk=st.booleans(),
+       variant=st.sampled_from([(1, 0, None), (2, 256, None), (2, 512, True), (2, 512, False)]),
        seed=st.integers(0, 10_000))
-def test_grouped_gemm_fuzz(P, sizes, n, k, nk, cg, seed):
+def test_grouped_gemm_fuzz(P, sizes, n, k, nk, variant, seed):
+    """(cta_group, tile_n, swap_tails): the 1-CTA, 256-wide and 512-wide
+    kernels, tails swapped or padded."""
     import torch
+    cg, tile_n, swap = variant
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(int).tolist()
     x = _bf16((max(offs[-1], 1), k), seed)[:offs[-1]]
     w = _bf16((len(sizes), k, n), seed + 1)
     tw = torch.from_numpy(np.ascontiguousarray(w.transpose(0, 2, 1)) if nk else w).cuda().bfloat16()
     y = P.grouped_gemm(torch.from_numpy(np.ascontiguousarray(x)).cuda().bfloat16(), offs, tw.contiguous(),
-                       w_layout=P.B_NK if nk else P.B_KN, cta_group=cg)
+                       w_layout=P.B_NK if nk else P.B_KN, cta_group=cg, tile_n=tile_n, swap_tails=swap)
     torch.cuda.synchronize()
     y = y.float().cpu().numpy()
     for e, want in enumerate(oracle.oracle_grouped_gemm(x, offs, w)):

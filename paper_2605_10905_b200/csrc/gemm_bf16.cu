@@ -773,6 +773,8 @@ cudaError_t grouped_wide_impl(const GroupedGemmArgs &g, cudaStream_t stream, int
                           : make_tmap_3d(wbase, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.k, g.n, cnt, g.k,
                                          g.k * g.n, BK, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     std::memset(gs, 0, sizeof(GroupedWideSched));
+    gs->x16 = make_tmap_2d(g.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, total_rows, g.k, g.k, BK, 16,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
     gs->n_groups = cnt;
     gs->num_n = (int)((g.n + WIDE_BN - 1) / WIDE_BN);
     gs->clc = clc;

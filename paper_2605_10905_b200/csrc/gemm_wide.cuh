@@ -50,6 +50,7 @@ static_assert(WIDE_SMEM <= 232448, "wide GEMM smem");
 struct GroupedWideSched {
   static constexpr bool kGrouped = true;
   CUtensorMap y[MAX_GROUPS];
+  CUtensorMap x16;                // X with 16-row boxes: a swapped tail loads only its swap_n/2 rows
   int tile_pref[MAX_GROUPS + 1];  // prefix over groups of m_tiles * num_n
   int mt[MAX_GROUPS];             // 256-row tiles of group e
   int row_off[MAX_GROUPS];
@@ -169,11 +170,21 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
           const uint32_t fb = full_target0 + 8 * stage;
-          if (leader) mbar_arrive_expect_tx(full_bar(stage), WIDE_STAGE_BYTES * 2);
+          // swapped tail: only the tail's swap_n / 2 X rows per CTA (16-row boxes), not a 128-row box
+          const int xrows = GROUPED && tc.swap_n ? tc.swap_n / 2 : BM_CTA;
+          if (leader) mbar_arrive_expect_tx(full_bar(stage), (WIDE_B_BYTES + xrows * BK * 2) * 2);
           const uint32_t sa = sbase + stage * WIDE_STAGE_BYTES;
           const uint32_t sb = sa + WIDE_A_BYTES;
           const int k0 = kb * BK;
-          tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+          if constexpr (GROUPED) {
+            if (tc.swap_n) {
+              for (int r = 0; r < xrows; r += 16) tma_load_2d_cg2(sa + r * BK * 2, &sched.x16, fb, k0, m0 + r);
+            } else {
+              tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+            }
+          } else {
+            tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if constexpr (GROUPED) {  // W[e] through the 3-D map: (n, k, e) for [G,K,N], (k, n, e) for [G,N,K]

@@ -29,7 +29,7 @@ for what in "$@"; do
         > "$OUT/fp8_ncu.log" 2>&1 ;;
     moe)
       timeout 900 $NCU --set full --import-source on --kernel-name-base demangled \
-        -k regex:GroupedSched -s 3 -c 1 -o "$OUT/moe" -f \
+        -k regex:"GroupedSched|GroupedWideSched" -s 3 -c 1 -o "$OUT/moe" -f \
         python bench.py --workload moe --steps 1 --warmup 3 --no-cpu > "$OUT/moe_ncu.log" 2>&1 ;;
     ln)
       timeout 900 $NCU --set full --import-source on -k regex:layernorm_cluster -s 3 -c 1 \

@@ -69,7 +69,10 @@ def traffic(key):
 class Clocks:
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.limit")
+    # clocks_event_reasons.active bit mask (nvml): reasons the per-reason columns do not cover
+    MASK = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+            0x100: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
@@ -81,7 +84,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             return
@@ -112,8 +115,16 @@ class Clocks:
         sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 8
-                          for i in range(4) if r[4 + i].lower().startswith("active")})
+        reasons = {names[i] for r in self.rows if len(r) >= 8
+                   for i in range(4) if r[4 + i].lower().startswith("active")}
+        for r in self.rows:
+            if len(r) >= 8:
+                try:
+                    bits = int(r[3], 16)
+                except ValueError:
+                    continue
+                reasons |= {v for k, v in self.MASK.items() if bits & k}
+        reasons = sorted(reasons)
         # "under load": samples drawing > 40% of the peak power seen (the 50-ms
         # sampler also catches the idle edges around a short timed region)
         pw = [float(r[2]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()
@@ -123,9 +134,12 @@ class Clocks:
         else:
             loaded = [s_ for s_ in sm if s_ > 500]
         loaded = loaded or sm
+        lim = [float(r[8]) for r in self.rows if len(r) >= 9 and r[8].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(loaded)) if loaded else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(sm)}
+                "samples": len(sm),
+                # the 1 kW cap: a clock below max with the draw at the limit is power, not a lock
+                "power_w_max": max(pw) if pw else None, "power_limit_w": max(lim) if lim else None}
 
 
 # ---------------------------------------------------------------------------

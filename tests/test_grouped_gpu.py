@@ -64,13 +64,15 @@ def test_grouped_ragged_full_oracle(P, cta_group, swap, tile_n, w_layout):
     assert np.all(got[:offs[0]] == 3.0) and np.all(got[offs[-1]:] == 3.0)
 
 
-def test_grouped_more_than_128_groups(P):
-    """More groups than one launch's parameter block holds (chunked launches)."""
+@pytest.mark.parametrize("tile_n", [256, 512])
+def test_grouped_more_than_128_groups(P, tile_n):
+    """More groups than one launch's parameter block holds (chunked launches),
+    for both tile widths."""
     import torch
     rng = np.random.default_rng(3)
     rows = list(rng.integers(0, 40, size=150))
     offs, x, w, tx, tw = _case(rows, 64, 64, 12)
-    got = P.grouped_gemm(tx, offs, tw).float().cpu().numpy()
+    got = P.grouped_gemm(tx, offs, tw, tile_n=tile_n).float().cpu().numpy()
     want = oracle.oracle_grouped_gemm(x, offs, w)
     for e in range(len(rows)):
         if rows[e]:

@@ -71,7 +71,10 @@ constexpr float LOG2E = 1.4426950408889634f;
 #endif
 constexpr int kDefaultEmu = 0;  // exp2 pairs (of 8) evaluated on the FMA pipe (0: measured fastest, tools/fa_sweep.py)
 constexpr int kDefaultEmuCg2 = 2;  // same, 2-CTA kernel
-constexpr int HEAD_BAND = 4;    // heads per scheduling band (K/V of a band stays in L2)
+#ifndef MIMW_FA_HEAD_BAND
+#define MIMW_FA_HEAD_BAND 8  // 1346-1349 vs 1333-1336 TFLOPS with 4 (tools/fa_ab.py; 1: 1325, 2: 1323, 16: 1343-1348)
+#endif
+constexpr int HEAD_BAND = MIMW_FA_HEAD_BAND;  // heads per scheduling band (K/V of a band stays in L2)
 
 struct Params {
   int bh;            // batch * heads

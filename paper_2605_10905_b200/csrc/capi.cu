@@ -914,11 +914,12 @@ int mimw_b200_gemm_mxfp8(const void *a, const void *sfa, const void *b, const vo
   return guarded([&] { gemm_mxfp8(a, sfa, b, sfb, c, m, n, k, 2, stream); });
 }
 
-// Test hook (not part of the public header): MXFP8 GEMM with forced cta_group.
+// Test hook (not part of the public header): MXFP8 GEMM with forced cta_group
+// (3: the 2-CTA kernel with 256 x 448 tiles, gemm_mxfp8_wide.cuh).
 int mimw_b200_gemm_mxfp8_ex(const void *a, const void *sfa, const void *b, const void *sfb, void *c,
                             int64_t m, int64_t n, int64_t k, int32_t cta_group, void *stream) {
   return guarded([&] {
-    require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
+    require(cta_group >= 1 && cta_group <= 3, MIMW_ERR_ARG, "cta_group must be 1, 2 or 3 (2-CTA, 448-wide tiles)");
     gemm_mxfp8(a, sfa, b, sfb, c, m, n, k, cta_group, stream);
   });
 }

@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(256) sf_tile_kernel(const uint8_t *__restrict_
   }
 }
 
+#include "gemm_mxfp8_wide.cuh"
+
 }  // namespace
 
 // Workspace: SFA atoms [ceil(m/128)][KG] x 512 B, then SFB atoms
@@ -402,7 +404,56 @@ cudaError_t launch_cg(const Mxfp8Args &g, cudaStream_t stream) {
   return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tSFA, tSFB, (int)g.m, (int)g.n, (int)g.k, kg, s);
 }
 
+// 256 x 448 pair tiles (gemm_mxfp8_wide.cuh): same scale-atom pre-pass and
+// workspace as the 256 x 224 kernel.
+cudaError_t launch_wide(const Mxfp8Args &g, cudaStream_t stream) {
+  const int kg = (int)((g.k + BK - 1) / BK);
+  const int num_m = (int)((g.m + 255) / 256);
+  const int num_n224 = (int)((g.n + BN - 1) / BN);
+  const int m128 = num_m * 2;
+  uint8_t *sfa_t = static_cast<uint8_t *>(g.workspace);
+  uint8_t *sfb_t = sfa_t + (size_t)m128 * kg * SFA_BYTES;
+  const int kb = (int)(g.k / 32);
+  sf_tile_kernel<<<dim3(m128 + 2 * num_n224, (kg + 31) / 32), 256, 0, stream>>>(
+      static_cast<const uint8_t *>(g.sfa), (int)g.m, static_cast<const uint8_t *>(g.sfb), (int)g.n, kb, kg, m128,
+      sfa_t, sfb_t);
+  CUtensorMap tA = make_tmap_2d(g.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.m, g.k, g.lda, BK, BM_CTA,
+                                CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tB = make_tmap_2d(g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.n, g.k, g.ldb, BK, BN / 2,
+                                CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap tC = make_tmap_2d(g.c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.m, g.n, g.ldc, EPI_COLS, 32,
+                                CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap tSFA = make_tmap_2d(sfa_t, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)m128 * kg * 2, 256, 256,
+                                  256, 2, CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap tSFB = make_tmap_2d(sfb_t, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)num_n224 * kg * 4, 256, 256,
+                                  256, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+  WideSched s;
+  s.num_m = num_m;
+  s.num_n = (int)((g.n + MW_BN - 1) / MW_BN);
+  s.group = 8;
+  s.clc = 1;
+  const int tiles = s.num_m * s.num_n;
+  auto kern = gemm_mxfp8_wide_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MW_SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles * 2, 1, 1);  // one cluster per tile; running clusters cancel the rest (CLC)
+  cfg.blockDim = dim3(MW_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = MW_SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tSFA, tSFB, (int)g.m, (int)g.n, (int)g.k, kg, s);
+}
+
 cudaError_t gemm_mxfp8_launch(const Mxfp8Args &g, cudaStream_t stream) {
+  static const int wide_env = getenv("MIMW_FP8_WIDE") ? atoi(getenv("MIMW_FP8_WIDE")) : 0;  // A/B knob
+  if (g.cta_group == 3 || (g.cta_group == 2 && wide_env != 0)) return launch_wide(g, stream);
   return g.cta_group == 1 ? launch_cg<1>(g, stream) : launch_cg<2>(g, stream);
 }
 

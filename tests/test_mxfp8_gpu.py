@@ -32,7 +32,7 @@ def _mx_operand(rows, k, seed):
 
 @pytest.mark.parametrize("m,n,k", [(128, 224, 128), (256, 448, 512), (300, 504, 1056), (1, 8, 32),
                                    (1024, 1024, 1024), (520, 8192, 160)])
-@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("cta_group", [1, 2, 3])  # 3: 2-CTA, 256 x 448 tiles
 def test_mxfp8_vs_dequant_oracle(P, m, n, k, cta_group):
     import torch
     qa, sfa = _mx_operand(m, k, m + k)
@@ -51,8 +51,10 @@ def test_mxfp8_vs_dequant_oracle(P, m, n, k, cta_group):
     assert oracle.rel_error_rows(got, want) <= TOL
 
 
-def test_mxfp8_8192_sampled_rows(P):
-    """configs[2] size (8192^3): row-sampled exact oracle on dequantised inputs."""
+@pytest.mark.parametrize("cta_group", [2, 3])
+def test_mxfp8_8192_sampled_rows(P, cta_group):
+    """configs[2] size (8192^3): row-sampled exact oracle on dequantised inputs
+    (cta_group 3: 256 x 448 tiles, whose last column tile is 128 wide)."""
     import torch
     m = n = k = 8192
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -62,7 +64,7 @@ def test_mxfp8_8192_sampled_rows(P):
     qb[(qb & 0x7F) == 0x7F] = 0x38
     sfa = torch.randint(120, 134, (m, k // 32), device="cuda", dtype=torch.uint8, generator=g)
     sfb = torch.randint(120, 134, (n, k // 32), device="cuda", dtype=torch.uint8, generator=g)
-    c = P.gemm_mxfp8(qa.view(torch.float8_e4m3fn), sfa, qb.view(torch.float8_e4m3fn), sfb)
+    c = P.gemm_mxfp8(qa.view(torch.float8_e4m3fn), sfa, qb.view(torch.float8_e4m3fn), sfb, cta_group=cta_group)
     torch.cuda.synchronize()
     rows = [0, 127, 128, 4097, 8191]
     a = oracle.mx_dequant(qa[rows].cpu().numpy(), sfa[rows].cpu().numpy())

@@ -432,6 +432,7 @@ cudaError_t launch_wide(const Mxfp8Args &g, cudaStream_t stream) {
   s.num_n = (int)((g.n + MW_BN - 1) / MW_BN);
   s.group = 8;
   s.clc = 1;
+  s.last_partial = (g.n % MW_BN) != 0 ? 1 : 0;
   const int tiles = s.num_m * s.num_n;
   auto kern = gemm_mxfp8_wide_kernel;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MW_SMEM);

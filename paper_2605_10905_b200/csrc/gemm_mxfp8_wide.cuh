@@ -34,8 +34,15 @@ constexpr uint32_t MW_TM_SF = 448;
 
 struct WideSched {
   int num_m, num_n, group, clc;  // num_m in 256-row tiles, num_n in 448-column tiles
+  int last_partial;              // the last column tile is narrower: dispatch its tiles last
   __device__ __forceinline__ void tile(int t, int &mt, int &nt) const {
-    const int per_group = group * num_n;
+    const int nfull = last_partial ? num_n - 1 : num_n;
+    if (t >= num_m * nfull) {  // the partial column tiles (cheaper) fill the last wave
+      mt = t - num_m * nfull;
+      nt = num_n - 1;
+      return;
+    }
+    const int per_group = group * nfull;
     const int g = t / per_group;
     const int first_m = g * group;
     const int gsize = min(num_m - first_m, group);

@@ -35,7 +35,7 @@ def evs(w):
 mma, w0, w4 = sorted(evs(9) + evs(10)), evs(0), evs(4)
 t0 = mma[0][0]
 names = {1: "S0", 2: "PV0", 3: "S1", 4: "PV1", 20: "V", 21: "S0i", 22: "PV0i", 23: "S1i", 24: "PV1i"}
-sm = {10: "sfull", 11: "ld", 12: "sfree", 13: "pvok", 14: "P"}
+sm = {10: "sfull", 15: "ld1", 16: "mx1", 11: "ld", 12: "sfree", 13: "pvok", 14: "P"}
 # group MMA events into steps at each S0 issue
 steps, cur = [], None
 for ts, c in mma:

@@ -609,7 +609,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 
 #include "attention_fwd_cg2.cuh"
 
-template <int EMU, bool SPLIT>
+template <int EMU>
 cudaError_t launch_cg2(const AttnArgs &a, const Params &p, cudaStream_t stream) {
   const uint64_t bh = (uint64_t)a.batch * a.heads;
   CUtensorMap tQ = make_tmap_3d(a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
@@ -620,7 +620,7 @@ cudaError_t launch_cg2(const AttnArgs &a, const Params &p, cudaStream_t stream) 
                                 (uint64_t)a.seq * D, 64, BKV, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   CUtensorMap tO = make_tmap_3d(a.o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D,
                                 (uint64_t)a.seq * D, 64, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  auto kern = attention_fwd_cg2_kernel<EMU, SPLIT>;
+  auto kern = attention_fwd_cg2_kernel<EMU>;
 #ifdef MIMW_FA_EVENTS
   constexpr int smem_total = C2_SMEM_TOTAL + 12 * 128 * 8;  // + the event log
 #else
@@ -695,21 +695,12 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   // than the one-CTA kernel on configs[3]: DESIGN.md §4.1)
   static const int cg2_env = getenv("MIMW_FA_CG2") ? atoi(getenv("MIMW_FA_CG2")) : 0;  // A/B knob
   if ((a.cta_group == 2 || cg2_env != 0) && a.max_ctas <= 0) {
-    if (cg2_env != 1) {  // key-split softmax warpgroups (MIMW_FA_CG2=1: alternate-step warpgroups)
-      switch (a.emu < 0 ? kDefaultEmuCg2 : a.emu) {
-        case 0: return launch_cg2<0, true>(a, p, stream);
-        case 1: return launch_cg2<1, true>(a, p, stream);
-        case 2: return launch_cg2<2, true>(a, p, stream);
-        case 3: return launch_cg2<3, true>(a, p, stream);
-        default: return launch_cg2<4, true>(a, p, stream);
-      }
-    }
     switch (a.emu < 0 ? kDefaultEmuCg2 : a.emu) {
-      case 0: return launch_cg2<0, false>(a, p, stream);
-      case 1: return launch_cg2<1, false>(a, p, stream);
-      case 2: return launch_cg2<2, false>(a, p, stream);
-      case 3: return launch_cg2<3, false>(a, p, stream);
-      default: return launch_cg2<4, false>(a, p, stream);
+      case 0: return launch_cg2<0>(a, p, stream);
+      case 1: return launch_cg2<1>(a, p, stream);
+      case 2: return launch_cg2<2>(a, p, stream);
+      case 3: return launch_cg2<3>(a, p, stream);
+      default: return launch_cg2<4>(a, p, stream);
     }
   }
   const int items = p.bh * p.nqb;

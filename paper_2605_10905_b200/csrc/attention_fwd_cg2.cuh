@@ -36,8 +36,8 @@ constexpr int C2_SLOT_BYTES = 64 * D * 2;     // 16 KiB: 64 keys x 128 d (K) or 
 constexpr int C2_SMEM_Q = 0;                  // 2 x 32 KiB Q tiles
 constexpr int C2_SMEM_KV = 2 * TILE_BYTES;
 constexpr int C2_SMEM_O = C2_SMEM_KV + C2_NSLOT * C2_SLOT_BYTES;   // 8 warps x 4 KiB O staging
-constexpr int C2_SMEM_RED = C2_SMEM_O + 8 * 4096;                  // per-step max exchange [2 parity][2 wg][128] f32
-constexpr int C2_SMEM_LRED = C2_SMEM_RED + 2 * 2 * 128 * 4;        // epilogue (l, m) exchange [2 wg][2][128] f32
+constexpr int C2_SMEM_RED = C2_SMEM_O + 8 * 4096;                  // per-step max hand-off [2 wg][128] f32
+constexpr int C2_SMEM_LRED = C2_SMEM_RED + 2 * 128 * 4;            // epilogue (l, m) exchange [2 wg][2][128] f32
 constexpr int C2_SMEM_BAR = C2_SMEM_LRED + 2 * 2 * 128 * 4;
 constexpr int C2_BAR_BYTES = 512;
 constexpr int C2_SMEM_TOTAL = C2_SMEM_BAR + C2_BAR_BYTES + 1024;
@@ -46,7 +46,7 @@ constexpr uint32_t C2_IDESC_S = idesc_bf16(256, BKV, 0, 0);   // Q (K-major) x K
 constexpr uint32_t C2_IDESC_PV = idesc_bf16(256, D, 0, 1);    // P (TMEM) x V (MN-major)
 constexpr uint32_t C2_TM_S = 0, C2_TM_P = 256, C2_TM_O = 384;
 
-template <int EMU, bool SPLIT>
+template <int EMU>
 __global__ void __launch_bounds__(C2_THREADS, 1)
 attention_fwd_cg2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Params p) {
@@ -103,9 +103,8 @@ attention_fwd_cg2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_c
     tma_prefetch_desc(&tmO);
     for (int b = 0; b < 2; ++b) {
       mbar_init(q_full(b), 1);
-      // SPLIT: all 8 softmax warps of both CTAs; else the 4 warps of warpgroup b, both CTAs
-      mbar_init(s_free(b), SPLIT ? 16 : 8);
-      mbar_init(p_full(b), SPLIT ? 16 : 8);
+      mbar_init(s_free(b), 8);   // the 4 warps of warpgroup b, both CTAs
+      mbar_init(p_full(b), 8);
       mbar_init(q_empty(b), 1);
       mbar_init(s_full(b), 1);
       mbar_init(pv_done(b), 1);
@@ -261,181 +260,6 @@ attention_fwd_cg2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_c
       }
     }
   }
-  } else if constexpr (SPLIT) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-    // ================= softmax / correction / epilogue, key-split =================
-    // Both warpgroups work on every KV step: warpgroup wg owns keys
-    // [64 wg, 64 wg + 64) of S (and P) and d-columns [64 wg, 64 wg + 64) of O.
-    // The row max of a step is combined through smem (one named barrier per
-    // warp pair q / q + 4, which share an SM sub-partition), so both halves
-    // apply the same reference max and O needs no cross-warpgroup rescale.
-    // Per step each warp loads 64 S columns, takes 64 exponentials and stores
-    // 32 packed P columns: the per-step chain is half the alternate-step one,
-    // and S / P double-buffering lets S(j+1) and PV(j-1) run under it.
-    const int q = warp & 3;    // TMEM lane quarter (rows q*32 ..)
-    const int wg = warp >> 2;  // key half
-    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const uint32_t lead_bars = map_to_rank(bars, 0);
-    const uint32_t red_s = sbase + C2_SMEM_RED;                     // [2 parity][2 wg][128 rows] partial max
-    float *lred = reinterpret_cast<float *>(smem + C2_SMEM_LRED);  // [2 wg][128 rows] l at the epilogue
-    const int trow = q * 32 + (int)lane;
-    uint32_t g = 0;
-    int n = 0;
-    for (int it = (int)cluster_id_x(); it < num_items; it = next_item(n++, lane == 0)) {
-      int bh, qb;
-      work_item(it, p, bh, qb);
-      int lo, hi;
-      pair_range(qb, lo, hi);
-      const int rt = qb * 2 * BQ + (int)rank * BQ;  // first row of this CTA's Q tile
-      const int row = rt + trow;
-      float m_used = -INFINITY;  // log2-domain reference max (identical in both warpgroups)
-      float l = 0.f;             // this warpgroup's share of the row sum
-      for (int j = lo; j <= hi; ++j, ++g) {
-        const uint32_t b = g & 1;
-        mbar_wait(s_full(b), (g >> 1) & 1, 30);
-        EV2(10);
-        tc_fence_after();
-        uint32_t s[64];
-        const uint32_t t_s = tmem + t_lane + C2_TM_S + b * 128 + wg * 64;
-        tmem_ld_32x32b_x32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(lead_bars + 80 + 8 * b);  // s_free(b) on the leader
-        EV2(11);
-        const int k0 = j * BKV + wg * 64;  // first key of this half
-        const bool need_mask = (p.causal && ((k0 + 63 > rt) || (k0 < rt + BQ - p.window))) ||
-                               (k0 + 64 > p.seq) || !p.scale_pos;
-        if (need_mask) {
-          if (!p.scale_pos) {
-#pragma unroll
-            for (int e = 0; e < 64; ++e) s[e] = __float_as_uint(__uint_as_float(s[e]) * p.scale_log2);
-          }
-          const int c_lo = p.causal ? row - p.window + 1 - k0 : -k0;
-          const int c_hi = (p.causal ? min(row, p.seq - 1) : p.seq - 1) - k0;
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e < c_lo || e > c_hi) s[e] = 0xff800000u;  // -inf
-        }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int e = 0; e < 64; e += 8) {
-#pragma unroll
-          for (int f = 0; f < 4; ++f)
-            m4[f] = fmax3(m4[f], __uint_as_float(s[e + 2 * f]), __uint_as_float(s[e + 2 * f + 1]));
-        }
-        const float sl = p.scale_pos ? p.scale_log2 : 1.f;
-        float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
-        // row max over both halves.  Slot parity b: the partner reads slot b of
-        // step g before it arrives at step g + 1's barrier, which this warp
-        // passes before it rewrites slot b at step g + 2.
-        st_shared_f32(red_s + (uint32_t)((b * 2 + wg) * 128 + trow) * 4, mx);
-        named_bar_sync(1 + q, 64);
-        mx = fmaxf(mx, ld_shared_f32(red_s + (uint32_t)((b * 2 + (wg ^ 1)) * 128 + trow) * 4));
-        EV2(18);
-        // online softmax: move the reference only when the max grows by > 8
-        // (2^8 headroom in fp32 / bf16 P), so O rescales are rare
-        float corr = 1.f;
-        bool rescale = false;
-        if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-          corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
-          rescale = (j != lo);
-          m_used = mx;
-        }
-        l *= corr;
-        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
-        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
-        uint64_t acc[4] = {0, 0, 0, 0};
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), sl2, nm2);
-          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
-          acc[e & 3] = f2_add(acc[e & 3], p2);
-          pk[e] = pack_bf16_2(p2);
-        }
-        {
-          float a0, a1, b0, b1;
-          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-          l += (a0 + a1) + (b0 + b1);
-        }
-        EV2(13);
-        // P_b was last read by PV(g - 2)
-        if (g >= 2) mbar_wait(pv_done(b), ((g >> 1) & 1) ^ 1, 32);
-        EV2(14);
-        if (__any_sync(0xffffffffu, rescale)) {
-          // O holds PV(.. g - 1) only once PV(g - 1) is done.  PV(g - 3) was
-          // waited for at step g - 1, so this parity wait cannot alias.
-          mbar_wait(pv_done(b ^ 1), ((g - 1) >> 1) & 1, 33);
-          tc_fence_after();
-          const uint32_t t_o = tmem + t_lane + C2_TM_O + wg * 64;
-#pragma unroll 1
-          for (int cc = 0; cc < 64; cc += 32) {
-            uint32_t o[32];
-            tmem_ld_32x32b_x32(t_o + cc, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            tmem_st_32x32b_x16(t_o + cc, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
-            tmem_st_32x32b_x16(t_o + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
-          }
-        } else {
-          tc_fence_after();
-        }
-        const uint32_t t_p = tmem + t_lane + C2_TM_P + b * 64 + wg * 32;
-        tmem_st_32x32b_x16(t_p, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-        tmem_st_32x32b_x16(t_p + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
-        tmem_st_wait();
-        EV2(17);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(lead_bars + 96 + 8 * b);  // p_full(b) on the leader
-        EV2(15);
-      }
-      // ---------------- epilogue: O / l, lse (warpgroup wg: O columns 64 wg ..) ----------------
-      const uint32_t g_last = g - 1;
-      if (g_last >= 1) mbar_wait(pv_done((g_last - 1) & 1), ((g_last - 1) >> 1) & 1, 41);
-      mbar_wait(pv_done(g_last & 1), (g_last >> 1) & 1, 40);
-      tc_fence_after();
-      uint32_t w[32];
-      {
-        const uint32_t t_o = tmem + t_lane + C2_TM_O + wg * 64;
-        uint32_t o[64];
-        tmem_ld_32x32b_x32(t_o, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-        tmem_ld_32x32b_x32(t_o + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(lead_bars + 112);  // o_free on the leader
-        lred[wg * 128 + trow] = l;
-        named_bar_sync(9 + q, 64);
-        const float lt = l + lred[(wg ^ 1) * 128 + trow];
-        named_bar_sync(9 + q, 64);  // both read before either rewrites (next item)
-        const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
-        if (wg == 0 && row < p.seq && p.lse != nullptr)
-          p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(lt)) * (1.0f / LOG2E);
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          w[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-      }
-      const uint32_t obuf = sbase + C2_SMEM_O + (uint32_t)warp * 4096;
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        st_shared_v4(obuf + lane * 128 + ((cc ^ (lane & 7)) << 4), w[4 * cc], w[4 * cc + 1], w[4 * cc + 2],
-                     w[4 * cc + 3]);
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0 && p.dbg != 1) {
-        tma_store_3d(&tmO, obuf, 64 * wg, rt + q * 32, bh);
-        bulk_commit();
-      }
-    }
-    if (lane == 0) bulk_wait<0>();
-    __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     // ================= softmax / correction / epilogue =================

@@ -1,6 +1,5 @@
 """Timeline of cluster 0 of the 2-CTA attention kernel (debug aid; run with
---build, which compiles an event build (-DMIMW_FA_EVENTS) into /tmp, and
-MIMW_FA_CG2=2 for the key-split variant or =1 for the alternate-step one).
+--build, which compiles an event build (-DMIMW_FA_EVENTS) into /tmp).
 Per KV step: when the leader issued S(j) / PV(j), and when CTA 0 / CTA 1
 softmax warp 0 saw S, released it, had the row max, finished the
 exponentials, had PV(j-2) done and published P (cycles)."""
@@ -61,8 +60,6 @@ for j in range(4, min(40, len(s_iss), len(pv_iss))):
     print(f"{j:3d} | {s_req[j] - t0:8d} {s_got[j] - t0:8d} {s_iss[j] - t0:8d} | {pv_req[j] - t0:8d} "
           f"{pv_got[j] - t0:8d} {pv_iss[j] - t0:8d} | {s_iss[j] - s_iss[j - 1]}")
 names = {10: "sfull", 16: "ld", 11: "sfree", 18: "exps", 19: "hand", 12: "pub", 13: "pack", 14: "pvok", 17: "st", 15: "P"}
-if os.environ.get("MIMW_FA_CG2") != "1":  # key-split softmax (default 2-CTA variant)
-    names = {10: "sfull", 11: "sfree", 18: "max", 13: "exps", 14: "pvok", 17: "st", 15: "P"}
 for r in (0, 1):
     ev = evs(r, 0)
     steps, cur = [], []

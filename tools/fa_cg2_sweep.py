@@ -1,7 +1,6 @@
 """FA forward timing, one-CTA kernel vs the 2-CTA kernel (cta_group=2) over
 the exp2-emulation split, in alternating order on one box:
-    python tools/fa_cg2_sweep.py [rounds]
-MIMW_FA_CG2=1 selects the alternate-step 2-CTA softmax variant."""
+    python tools/fa_cg2_sweep.py [rounds]"""
 import os
 import sys
 import time

@@ -190,6 +190,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         mbar_wait(sched_empty(ss), ((n >> 1) & 1) ^ 1, 12);
         sched_slot[ss] = it < num_items ? it : -1;
         mbar_arrive(sched_full(ss));
+        EV(33);
         if (it >= num_items) {
           // self-reset of this launch's counter slot: the last CTA to retire
           // (after every CTA's final claim, fenced) zeroes it for the next
@@ -387,6 +388,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     for (int n = 0;; ++n) {
       const int ss = n & 1;
       mbar_wait(sched_full(ss), (n >> 1) & 1, 28);
+      EV(32);
       const int it = sched_slot[ss];
       __syncwarp();
       if (lane == 0) mbar_arrive(sched_empty(ss));

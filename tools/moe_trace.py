@@ -41,8 +41,8 @@ for e in range(E):
     w[e] = (torch.rand((K, N), device="cuda", generator=g) * 2 - 1).bfloat16()
 y = torch.empty((int(offs[-1]), N), device="cuda", dtype=torch.bfloat16)
 # host copy of the kernel's tile order (chunk 1: groups in turn, N-tiles outer, M-tiles inner);
-# MIMW_MOE_WIDE=1: 256 x 512 tiles with padded tails
-WIDE = os.environ.get("MIMW_MOE_WIDE", "0") != "0"
+# MIMW_MOE_WIDE (default 1): 256 x 512 tiles
+WIDE = os.environ.get("MIMW_MOE_WIDE", "1") != "0"
 nn = (N + 511) // 512 if WIDE else (N + 255) // 256
 tiles = []
 for e in range(E):

@@ -102,6 +102,10 @@ int main() {
     run<0, 128>(w, o, c); run<1, 128>(w, o, c); run<2, 128>(w, o, c); run<3, 128>(w, o, c);
     run<0, 64>(w, o, c); run<2, 64>(w, o, c); run<3, 64>(w, o, c);
   }
+  for (int w : {4}) {
+    run<0, 64>(w, o, c); run<2, 64>(w, o, c); run<3, 64>(w, o, c);
+    run<0, 128>(w, o, c); run<3, 128>(w, o, c);
+  }
   for (int w : {2, 3})
     for (int dummy = 0; dummy < 1; ++dummy) {
       run<2, 128, 1>(w, o, c); run<3, 128, 1>(w, o, c); run<4, 128, 1>(w, o, c);

@@ -59,10 +59,6 @@ constexpr int SMEM_Q = 0;
 constexpr int SMEM_KV = 2 * TILE_BYTES;
 constexpr int SMEM_O = SMEM_KV + NSLOT * TILE_BYTES;  // O staging: 8 softmax warps x 4 KiB (32 rows x 64 cols bf16)
 constexpr int SMEM_BAR = SMEM_O + 8 * 4096;
-// key-split kernel: 16 warps x 1 KiB O boxes, then the max / row-sum exchange areas
-constexpr int KS_RED = 16 * 1024;            // [2 h][2 parity][2 half][128] f32 (4 KiB)
-constexpr int KS_LRED = KS_RED + 4096;       // [2 h][2 half][128] f32 (2 KiB)
-static_assert(KS_LRED + 2048 <= 8 * 4096, "key-split exchange areas");
 constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 constexpr uint32_t IDESC_S = idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t IDESC_PV = idesc_bf16(BQ, D, 0, 1);    // P (TMEM) x V (MN-major)
@@ -75,7 +71,6 @@ constexpr float LOG2E = 1.4426950408889634f;
 #endif
 constexpr int kDefaultEmu = 0;  // exp2 pairs (of 8) evaluated on the FMA pipe (0: measured fastest, tools/fa_sweep.py)
 constexpr int kDefaultEmuCg2 = 2;  // same, 2-CTA kernel
-constexpr int kDefaultEmuKs = 2;   // same, key-split kernel
 #ifndef MIMW_FA_HEAD_BAND
 #define MIMW_FA_HEAD_BAND 8  // 1346-1349 vs 1333-1336 TFLOPS with 4 (tools/fa_ab.py; 1: 1325, 2: 1323, 16: 1343-1348)
 #endif
@@ -115,12 +110,8 @@ __device__ __forceinline__ void work_item(int idx, const Params &p, int &bh, int
   bh = band * HEAD_BAND + r % heads_in_band;
 }
 
-// KS = true: four softmax warpgroups (warps 0-15), two per Q tile, each on
-// 64 of the 128 keys of every KV step (the row max is combined through smem
-// per step); control warps 16-19.  Twice the softmax warps per SM
-// sub-partition hide the exponentials' latency better (tools/exp_rate.cu).
-template <int EMU, bool KS>
-__global__ void __launch_bounds__(KS ? 640 : NUM_THREADS, 1)
+template <int EMU>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
 attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -144,20 +135,19 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
   const int warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
   const int num_items = p.bh * p.nqb;
-  constexpr int SMW = KS ? 16 : 8;  // softmax warps; control warps SMW .. SMW + 3
 #ifdef MIMW_FA_EVENTS
   // event log of CTA 0 (tools/fa_events.py): warps 0, 4 (softmax lane quarter 0) and 9 (MMA)
   int ev_n = 0;
 #define EV(code)                                                                          \
   do {                                                                                    \
-    if (blockIdx.x == 0 && lane == 0 && ev_n < 1024 && p.trace && warp < 12)              \
+    if (blockIdx.x == 0 && lane == 0 && ev_n < 1024 && p.trace)                           \
       p.trace[warp * 1024 + ev_n++] = ((unsigned long long)clock64() << 8) | (code);     \
   } while (0)
 #else
 #define EV(code) do {} while (0)
 #endif
 
-  if (warp == SMW && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
@@ -165,32 +155,29 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       mbar_init(q_full(h), 1);
       mbar_init(q_empty(h), 1);
       mbar_init(s_full(h), 1);
-      mbar_init(p_full(h), KS ? 8 : 4);
+      mbar_init(p_full(h), 4);
       mbar_init(o_done(h), 1);
       mbar_init(sched_full(h), 1);
-      mbar_init(sched_empty(h), 2 + SMW);  // 2 MMA warps + the softmax warps
+      mbar_init(sched_empty(h), 10);  // 2 MMA warps + 8 softmax warps
     }
-    mbar_init(s_free, KS ? 8 : 4);
+    mbar_init(s_free, 4);
     for (int s = 0; s < NSLOT; ++s) {
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
     }
     fence_mbar_init();
   }
-  if (warp == SMW + 1) tmem_alloc<1>(tmem_slot, 512);
+  if (warp == 9) tmem_alloc<1>(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
 
-  if (warp >= SMW) {
+  if (warp >= 8) {
   // control warpgroup gives registers to the two softmax warpgroups.  Budget:
   // the pool only holds what dec releases: 8 warps x (208-168) <= 4 x (168-88).
-  if constexpr (KS)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
-  else
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
-  if (warp == SMW) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+  if (warp == 8) {
     // ================= scheduler + TMA producer =================
     if (lane == 0) {
       int slot = 0;
@@ -253,11 +240,11 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         }
       }
     }
-  } else if (warp == SMW + 1 || warp == SMW + 2) {
+  } else if (warp == 9 || warp == 10) {
     // ================= MMA issuers (S: warp 9, PV: warp 10) =================
     // The whole warp runs the schedule (so descriptor math stays on the
     // uniform datapath); one elected lane issues tcgen05.mma / commit.
-    const bool s_role = warp == SMW + 1;
+    const bool s_role = warp == 9;
     uint32_t ring = 0;  // K/V ring positions consumed so far (K_j at 2(j-lo), V_j at 2(j-lo)+1)
     uint32_t q_phase[2] = {0, 0}, sf_phase = 0;
     uint32_t p_phase0 = 0, p_phase1 = 0;
@@ -384,180 +371,6 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
       for (int e = 0; e < 8; ++e) p.trace[((size_t)blockIdx.x * 12 + warp) * 8 + e] = mt_acc[e];
 #endif
   }
-  } else if constexpr (KS) {
-    // register budget (640 threads compiled at 96): the control warpgroup's
-    // 4 x 32 x (96 - 64) released registers cover 16 x 32 x (104 - 96)
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
-    // ================= softmax / correction / epilogue (key-split) =================
-    // warpgroup wg: Q tile h = wg / 2, keys [64 half, 64 half + 64) of every
-    // KV tile (half = wg % 2), O_h columns [64 half, 64 half + 64).  Warps q
-    // and q + 4 of a tile's two warpgroups own the same 32 rows and the same
-    // SM sub-partition; they combine the row max once per step through smem
-    // (named barrier 1 + 4 h + q), so both halves use the same reference max.
-    const int wg = warp >> 2;
-    const int h = wg >> 1;
-    const int half = wg & 1;
-    const int q = warp & 3;
-    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const uint32_t t_s = tmem + t_lane + TM_S + 64 * half;
-    const uint32_t t_p = tmem + t_lane + TM_P + h * 64 + 32 * half;
-    const uint32_t t_o = tmem + t_lane + TM_O + h * 128 + 64 * half;
-    const uint32_t red_s = sbase + SMEM_O + KS_RED;    // [2 h][2 parity][2 half][128] partial max
-    const uint32_t lred_s = sbase + SMEM_O + KS_LRED;  // [2 h][2 half][128] row-sum shares
-    const uint32_t bar_x = 1 + 4 * h + q;
-    const int trow = q * 32 + (int)lane;
-    uint32_t s_phase = 0;
-    uint32_t od_count = 0;  // o_done[h] phases consumed (one per PV_h)
-    uint32_t xc = 0;        // max exchanges so far (slot parity)
-    for (int n = 0;; ++n) {
-      const int ss = n & 1;
-      mbar_wait(sched_full(ss), (n >> 1) & 1, 28);
-      const int it = sched_slot[ss];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sched_empty(ss));
-      if (it < 0) break;
-      int bh, qb;
-      work_item(it, p, bh, qb);
-      const int rt = qb * 2 * BQ + h * BQ;  // first row of this Q tile
-      const int row = rt + trow;
-      if (rt >= p.seq) continue;  // tile beyond seq: never loaded, nothing to release
-      int lo, hi;
-      kv_range(rt, p, lo, hi);
-      float m_used = -INFINITY;  // log2-domain reference max (identical in both halves)
-      float l = 0.f;             // this half's share of the row sum
-      for (int j = lo; j <= hi; ++j) {
-        mbar_wait(s_full(h), s_phase, 30 + h);
-        s_phase ^= 1;
-        tc_fence_after();
-        uint32_t s[64];
-        tmem_ld_32x32b_x32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_free);
-        const int k0 = j * BKV + 64 * half;  // first key of this half
-        const bool need_mask = (p.causal && ((k0 + 63 > rt) || (k0 < rt + BQ - p.window))) ||
-                               (k0 + 64 > p.seq) || !p.scale_pos;
-        if (need_mask) {
-          if (!p.scale_pos) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) * p.scale_log2);
-          }
-          const int c_lo = p.causal ? row - p.window + 1 - k0 : -k0;
-          const int c_hi = (p.causal ? min(row, p.seq - 1) : p.seq - 1) - k0;
-#pragma unroll
-          for (int c = 0; c < 64; ++c)
-            if (c < c_lo || c > c_hi) s[c] = 0xff800000u;  // -inf
-        }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < 64; c += 8) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            m4[e] = fmax3(m4[e], __uint_as_float(s[c + 2 * e]), __uint_as_float(s[c + 2 * e + 1]));
-        }
-        const float sl = p.scale_pos ? p.scale_log2 : 1.f;
-        float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sl;
-        // slot parity xb: the partner reads slot xb of this step before it
-        // reaches the next step's barrier, which this warp passes before it
-        // rewrites slot xb two steps later
-        const uint32_t xb = xc & 1;
-        ++xc;
-        st_shared_f32(red_s + (uint32_t)(((h * 2 + xb) * 2 + half) * 128 + trow) * 4, mx);
-        named_bar_sync(bar_x, 64);
-        mx = fmaxf(mx, ld_shared_f32(red_s + (uint32_t)(((h * 2 + xb) * 2 + (half ^ 1)) * 128 + trow) * 4));
-        // online softmax: only move the reference max when it grows by > 8
-        float corr = 1.f;
-        bool rescale = false;
-        if (mx > m_used + 8.f || (m_used == -INFINITY && mx > -INFINITY)) {
-          corr = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
-          rescale = (j != lo);
-          m_used = mx;
-        }
-        l *= corr;
-        const float nm = (m_used == -INFINITY) ? 0.f : -m_used;
-        const uint64_t sl2 = f2_pack(sl, sl), nm2 = f2_pack(nm, nm);
-        uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), sl2, nm2);
-          const uint64_t p2 = ((e & 7) < EMU) ? ex2_poly2(x2) : ex2_mufu2(x2);
-          acc[e & 3] = f2_add(acc[e & 3], p2);
-          s[e] = pack_bf16_2(p2);  // P packed in place (s[2e], s[2e+1] already read)
-        }
-        {
-          float a0, a1, b0, b1;
-          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-          l += (a0 + a1) + (b0 + b1);
-        }
-        // PV_h(j-1) must be complete before P_h is overwritten / O_h rescaled
-        if (j > lo) {
-          mbar_wait(o_done(h), od_count & 1, 32 + h);
-          ++od_count;
-          tc_fence_after();
-        }
-        if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
-            uint32_t o[32];
-            tmem_ld_32x32b_x32(t_o + c, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            tmem_st_32x32b_x16(t_o + c, *reinterpret_cast<uint32_t(*)[16]>(&o[0]));
-            tmem_st_32x32b_x16(t_o + c + 16, *reinterpret_cast<uint32_t(*)[16]>(&o[16]));
-          }
-        }
-        tmem_st_32x32b_x16(t_p, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
-        tmem_st_32x32b_x16(t_p + 16, *reinterpret_cast<uint32_t(*)[16]>(&s[16]));
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full(h));
-      }
-      // ---------------- epilogue: O / l, lse ----------------
-      mbar_wait(o_done(h), od_count & 1, 40 + h);
-      ++od_count;
-      tc_fence_after();
-      // row sum over both halves; the partner reads this slot before it can
-      // reach its next epilogue (it passes this pair's per-step barriers first)
-      st_shared_f32(lred_s + (uint32_t)((h * 2 + half) * 128 + trow) * 4, l);
-      named_bar_sync(bar_x, 64);
-      const float lt = l + ld_shared_f32(lred_s + (uint32_t)((h * 2 + (half ^ 1)) * 128 + trow) * 4);
-      const float inv_l = (lt > 0.f) ? 1.f / lt : 0.f;
-      if (half == 0 && row < p.seq && p.lse != nullptr)
-        p.lse[(size_t)bh * p.seq + row] = (m_used + __log2f(lt)) * (1.0f / LOG2E);
-      // O / l through a per-warp 1 KiB box (32 rows x 16 columns) and TMA stores
-      const uint32_t obuf = sbase + SMEM_O + (uint32_t)warp * 1024;
-#pragma unroll 1
-      for (int c = 0; c < 64; c += 32) {
-        uint32_t o[32];
-        tmem_ld_32x32b_x32(t_o + c, o);
-        tmem_ld_wait();
-        uint32_t w[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          w[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          if (lane == 0) bulk_wait_read<0>();  // the previous store from this box has read it
-          __syncwarp();
-          st_shared_v4(obuf + lane * 32, w[8 * b], w[8 * b + 1], w[8 * b + 2], w[8 * b + 3]);
-          st_shared_v4(obuf + lane * 32 + 16, w[8 * b + 4], w[8 * b + 5], w[8 * b + 6], w[8 * b + 7]);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0 && p.dbg != 1) {
-            tma_store_3d(&tmO, obuf, 64 * half + c + 16 * b, rt + q * 32, bh);
-            bulk_commit();
-          }
-        }
-      }
-      tc_fence_before();  // O_h read before the next item's first PV_h overwrites it
-    }
-    if (lane == 0) bulk_wait<0>();
-    __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     // ================= softmax / correction / epilogue (WG h) =================
@@ -790,7 +603,7 @@ attention_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 
   tc_fence_before();
   __syncthreads();
-  if (warp == SMW + 1) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<1>(tmem, 512);
   }
@@ -902,36 +715,19 @@ cudaError_t attention_fwd_launch(const AttnArgs &a, cudaStream_t stream) {
   // zeroes its slot (no per-launch allocation or memset).
   p.work_counter = fa_counter_slot();
   cudaError_t e = p.work_counter ? cudaSuccess : cudaErrorMemoryAllocation;
-  // key-split kernel (KS): A/B knob MIMW_FA_KS, or the cta_group argument 3
-  static const int ks_env = getenv("MIMW_FA_KS") ? atoi(getenv("MIMW_FA_KS")) : 0;
-  const bool ks = ks_env != 0 || a.cta_group == 3;
-  CUtensorMap tO16;
-  if (ks)
-    tO16 = make_tmap_3d(a.o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, a.seq, bh, D, (uint64_t)a.seq * D, 16, 32, 1,
-                        CU_TENSOR_MAP_SWIZZLE_NONE);
-  auto launch = [&](auto kern, bool is_ks) {
+  auto launch = [&](auto kern) {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e2 != cudaSuccess) return e2;
-    kern<<<grid, is_ks ? 640 : NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, is_ks ? tO16 : tO, p);
+    kern<<<grid, NUM_THREADS, SMEM_TOTAL, stream>>>(tQ, tK, tV, tO, p);
     return cudaGetLastError();
   };
   if (e == cudaSuccess) {
-    if (ks) {
-      switch (a.emu < 0 ? kDefaultEmuKs : a.emu) {
-        case 0: e = launch(attention_fwd_kernel<0, true>, true); break;
-        case 1: e = launch(attention_fwd_kernel<1, true>, true); break;
-        case 2: e = launch(attention_fwd_kernel<2, true>, true); break;
-        case 3: e = launch(attention_fwd_kernel<3, true>, true); break;
-        default: e = launch(attention_fwd_kernel<4, true>, true); break;
-      }
-    } else {
-      switch (a.emu < 0 ? kDefaultEmu : a.emu) {
-        case 0: e = launch(attention_fwd_kernel<0, false>, false); break;
-        case 1: e = launch(attention_fwd_kernel<1, false>, false); break;
-        case 2: e = launch(attention_fwd_kernel<2, false>, false); break;
-        case 3: e = launch(attention_fwd_kernel<3, false>, false); break;
-        default: e = launch(attention_fwd_kernel<4, false>, false); break;
-      }
+    switch (a.emu < 0 ? kDefaultEmu : a.emu) {
+      case 0: e = launch(attention_fwd_kernel<0>); break;
+      case 1: e = launch(attention_fwd_kernel<1>); break;
+      case 2: e = launch(attention_fwd_kernel<2>); break;
+      case 3: e = launch(attention_fwd_kernel<3>); break;
+      default: e = launch(attention_fwd_kernel<4>); break;
     }
   }
   return e;

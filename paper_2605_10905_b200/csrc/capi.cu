@@ -1035,7 +1035,7 @@ int mimw_b200_attention_fwd_ex(const void *q, const void *k, const void *v, void
   return guarded([&] {
     if (!attention_device_checks(q, k, v, o, batch, heads, seq, 128, window)) return;
     require(emu >= -1 && emu <= 4 && max_ctas >= 0, MIMW_ERR_ARG, "bad emu / max_ctas");
-    require(cta_group >= 1 && cta_group <= 3, MIMW_ERR_ARG, "cta_group must be 1, 2 or 3 (one-CTA key-split kernel)");
+    require(cta_group == 1 || cta_group == 2, MIMW_ERR_ARG, "cta_group must be 1 or 2");
     mimw::AttnArgs a{};
     a.q = q;
     a.k = k;

@@ -30,7 +30,10 @@ constexpr int WIDE_THREADS = 64 + 32 * WIDE_EPI_WARPS;
 constexpr int WIDE_A_BYTES = BM_CTA * BK * 2;          // 16 KiB
 constexpr int WIDE_B_BYTES = WIDE_NB_CTA * BK * 2;     // 32 KiB
 constexpr int WIDE_STAGE_BYTES = WIDE_A_BYTES + WIDE_B_BYTES;
-constexpr int WIDE_STAGES = 4;
+#ifndef MIMW_WIDE_STAGES
+#define MIMW_WIDE_STAGES 4
+#endif
+constexpr int WIDE_STAGES = MIMW_WIDE_STAGES;
 constexpr int WIDE_EPI_BUF = 32 * EPI_COLS * 2;        // 2 KiB: 32 rows x 32 bf16
 constexpr int WIDE_EPI_BYTES = WIDE_EPI_WARPS * 2 * WIDE_EPI_BUF;
 constexpr int WIDE_BAR_OFF = WIDE_STAGES * WIDE_STAGE_BYTES + WIDE_EPI_BYTES;

@@ -255,7 +255,7 @@ static void host_gemm_host_staged(const std::vector<const float *> &a_parts,
     check_cuda(cudaEventSynchronize(e_d[ci].e), "gemm execution");
     const float *hc = static_cast<const float *>(mimw::pinned_slot(7 + (ci & 1), (size_t)achunk * n * 4));
     mimw::host_parallel_for(rows, [&](int64_t lo, int64_t hi) {
-      std::memcpy(c + (r0 + lo) * n, hc + lo * n, sizeof(float) * (size_t)(hi - lo) * n);
+      mimw::host_copy_f32(c + (r0 + lo) * n, hc + lo * n, (hi - lo) * n);
     });
   };
   for (int ci = 0; ci < nchunks; ++ci) {

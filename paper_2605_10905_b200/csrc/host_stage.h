@@ -18,6 +18,10 @@ void host_rows_to_bf16(const float *src, int64_t ld_src, int64_t rows, int64_t c
 void host_rows_bf16_to_f32(const uint16_t *src, int64_t ld_src, int64_t rows, int64_t cols, float *dst,
                            int64_t ld_dst);
 
+// dst[0, n) = src[0, n) with streaming stores (the drain of a pinned result
+// slot into the caller's pageable buffer)
+void host_copy_f32(float *dst, const float *src, int64_t n);
+
 // Runs f(lo, hi) over [0, n) split across the process-wide host thread pool
 // (the caller participates) and returns when every range is done.
 void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)> &f);

@@ -491,20 +491,29 @@ __global__ void attention_bwd_prep(const __nv_bfloat16 *o, const __nv_bfloat16 *
   }
 }
 
-// dQ[bh, s, d] = bf16(scale * dQacc^T[bh, d, s]) through 32 x 32 smem tiles
-__global__ void attention_bwd_dq(const float *acc, __nv_bfloat16 *dq, int seq, int ld, float scale) {
-  __shared__ float tile[32][33];
+// dQ[bh, s, d] = bf16(scale * dQacc^T[bh, d, s]) through 64 (d) x 32 (s) smem
+// tiles: 128-B coalesced loads along s, and each warp stores one dQ row
+// segment of 64 d as bf16x2 (128 B), so both sides move whole lines.
+__global__ void __launch_bounds__(256) attention_bwd_dq(const float *acc, __nv_bfloat16 *dq, int seq, int ld,
+                                                        float scale) {
+  __shared__ float tile[64][33];
   const int b = blockIdx.z;
-  const int s0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+  const int s0 = blockIdx.x * 32, d0 = blockIdx.y * 64;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 8 warps
   const float *src = acc + (size_t)b * D * ld;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int s = s0 + threadIdx.x;
-    tile[r][threadIdx.x] = s < seq ? src[(size_t)(d0 + r) * ld + s] : 0.f;
+#pragma unroll
+  for (int r = w; r < 64; r += 8) {
+    const int s = s0 + lane;
+    tile[r][lane] = s < seq ? src[(size_t)(d0 + r) * ld + s] : 0.f;
   }
   __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+#pragma unroll
+  for (int r = w; r < 32; r += 8) {
     const int s = s0 + r;
-    if (s < seq) dq[((size_t)b * seq + s) * D + d0 + threadIdx.x] = __float2bfloat16_rn(tile[threadIdx.x][r] * scale);
+    if (s < seq) {
+      const __nv_bfloat162 v = __floats2bfloat162_rn(tile[2 * lane][r] * scale, tile[2 * lane + 1][r] * scale);
+      reinterpret_cast<__nv_bfloat162 *>(dq + ((size_t)b * seq + s) * D + d0)[lane] = v;
+    }
   }
 }
 
@@ -568,7 +577,7 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
     }
   }
   if (e == cudaSuccess) {
-    attention_bwd_dq<<<dim3((seq + 31) / 32, D / 32, bh), dim3(32, 8), 0, stream>>>(
+    attention_bwd_dq<<<dim3((seq + 31) / 32, D / 64, bh), 256, 0, stream>>>(
         acc, static_cast<__nv_bfloat16 *>(a.dq), seq, npad, (float)a.scale);
     e = cudaGetLastError();
   }

@@ -399,6 +399,16 @@ def bench_gemm(args, rank, ws, local):
         cublas = round(flop * args.steps / csecs / 1e12, 2)
     except Exception as e:  # noqa: BLE001
         cublas = f"unavailable: {type(e).__name__}"
+    # the design alternatives on the same operands, same box: the 256x256 pair
+    # tile, and clusters of two pairs sharing each B k-block by TMA multicast
+    # (north_star's "2-CTA cluster mode with TMA multicast")
+    alts = {}
+    for name, kw in (("tile_256x256", dict(tile_n=256)), ("tma_multicast_two_pairs", dict(cta_group=4))):
+        try:
+            asecs = timed(lambda kw=kw: P.gemm(a, b, out=c, **kw), args.steps, args.warmup, ws, stream)
+            alts[name] = round(flop * args.steps / asecs / 1e12, 2)
+        except Exception as e:  # noqa: BLE001
+            alts[name] = f"unavailable: {type(e).__name__}"
 
     # end to end through the reference-facing C-ABI with HOST f32 buffers
     # (mimw_b200_oracle_gemm: H2D of A, B, bf16 staging, GEMM, D2H of C), with
@@ -459,6 +469,7 @@ def bench_gemm(args, rank, ws, local):
                      "frac_of_spec_2250": round(achieved / 2250.0, 4),
                      "traffic": traffic("gemm_bf16_8192"),
                      "cublas_tflops_same_box": cublas,
+                     "alternatives_tflops_same_box": alts,
                      "algorithmic_bytes_min": 2.0 * (GEMM_M * GEMM_K + GEMM_K * GEMM_N + GEMM_M * GEMM_N),
                      "algorithmic_flop_per_launch": flop},
         "e2e": e2e,

@@ -460,34 +460,48 @@ attention_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
 }
 
 // D = rowsum(dO o O) and lse2 = lse * log2(e), both zero padded to nq * 64
-// per head; one warp per row.
+// per head; one warp per PREP_ROWS rows, every row's loads issued before the
+// first reduction (more bytes in flight per warp than one row at a time).
+constexpr int PREP_ROWS = 4;
 __global__ void attention_bwd_prep(const __nv_bfloat16 *o, const __nv_bfloat16 *dout, const float *lse,
                                    float *lse2, float *dvec, int bh, int seq, int npad) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (warp >= bh * npad) return;
-  const int b = warp / npad, s = warp % npad;
-  float acc = 0.f;
-  float l2 = 0.f;
-  if (s < seq) {
-    const size_t row = (size_t)b * seq + s;
-    const uint2 ov = reinterpret_cast<const uint2 *>(o + row * D)[lane];
-    const uint2 dv = reinterpret_cast<const uint2 *>(dout + row * D)[lane];
-    const __nv_bfloat162 *o2 = reinterpret_cast<const __nv_bfloat162 *>(&ov);
-    const __nv_bfloat162 *d2 = reinterpret_cast<const __nv_bfloat162 *>(&dv);
+  const int r0 = warp * PREP_ROWS;  // npad is a multiple of 64, so a warp's rows share one head
+  if (r0 >= bh * npad) return;
+  const int b = r0 / npad, s0 = r0 % npad;
+  uint2 ov[PREP_ROWS], dv[PREP_ROWS];
+  float l2[PREP_ROWS];
+#pragma unroll
+  for (int i = 0; i < PREP_ROWS; ++i) {
+    const int s = s0 + i;
+    ov[i] = make_uint2(0, 0);
+    dv[i] = make_uint2(0, 0);
+    l2[i] = 0.f;
+    if (s < seq) {
+      const size_t row = (size_t)b * seq + s;
+      ov[i] = reinterpret_cast<const uint2 *>(o + row * D)[lane];
+      dv[i] = reinterpret_cast<const uint2 *>(dout + row * D)[lane];
+      l2[i] = lse[row] * LOG2E;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PREP_ROWS; ++i) {
+    const __nv_bfloat162 *o2 = reinterpret_cast<const __nv_bfloat162 *>(&ov[i]);
+    const __nv_bfloat162 *d2 = reinterpret_cast<const __nv_bfloat162 *>(&dv[i]);
+    float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const float2 of = __bfloat1622float2(o2[e]);
       const float2 df = __bfloat1622float2(d2[e]);
       acc += of.x * df.x + of.y * df.y;
     }
-    l2 = lse[row] * LOG2E;
-  }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) {
-    dvec[(size_t)b * npad + s] = acc;
-    lse2[(size_t)b * npad + s] = l2;
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == i) {
+      dvec[(size_t)b * npad + s0 + i] = acc;
+      lse2[(size_t)b * npad + s0 + i] = l2[i];
+    }
   }
 }
 
@@ -540,7 +554,7 @@ cudaError_t attention_bwd_launch(const AttnBwdArgs &a, cudaStream_t stream) {
   e = cudaMemsetAsync(acc, 0, acc_bytes, stream);
   if (e == cudaSuccess) {
     const int rows = bh * npad;
-    attention_bwd_prep<<<(rows + 7) / 8, 256, 0, stream>>>(
+    attention_bwd_prep<<<(rows + 8 * PREP_ROWS - 1) / (8 * PREP_ROWS), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16 *>(a.o), static_cast<const __nv_bfloat16 *>(a.dout), a.lse, lse2,
         dvec, bh, seq, npad);
     e = cudaGetLastError();

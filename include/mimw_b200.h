@@ -190,8 +190,10 @@ int mimw_b200_oracle_attention_heads(const float *q, const float *k, const float
 #define MIMW_WINDOW_NONCAUSAL 0
 
 /* Same with a precision: MIMW_PREC_BF16 (the tcgen05 kernel on bf16 inputs,
- * rel-err ~3e-3, the north-star 1e-2 bar) or MIMW_PREC_F32 (the reference's own
- * 1e-4, acceptance.cpp:333-355). */
+ * rel-err ~3e-3, the north-star 1e-2 bar), MIMW_PREC_F32_BF16X3 (split-bf16 x3
+ * scores and P.V on the tcgen05 GEMM, softmax in f32: the reference's own 1e-4,
+ * acceptance.cpp:333-355) or MIMW_PREC_F32 (f64 scores on CUDA cores, one CTA
+ * per query row: the reference's arithmetic, for callers that want it). */
 int mimw_b200_oracle_attention_ex(const float *q, const float *k, const float *v, float *o,
                                   float *lse, int64_t seq, int64_t d, int64_t w, double scale,
                                   int32_t precision);

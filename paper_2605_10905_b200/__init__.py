@@ -142,8 +142,10 @@ def oracle_attention(q, k, v, w: int, scale: float, with_lse: bool = False,
                      precision: int = PREC_BF16):
     """``void oracle_attention(q, k, v, int w, double scale, Tile *o)``
     (oracles.hpp:35-37): windowed causal softmax attention of one [S, D] head.
-    ``precision=PREC_F32`` holds the reference's own 1e-4 (the oracle's f64
-    arithmetic on CUDA cores); the default is the bf16 tcgen05 kernel (1e-2)."""
+    ``precision=PREC_F32_BF16X3`` holds the reference's own 1e-4 on the
+    tcgen05 tensor cores (split-bf16 x3 scores and P.V, f32 softmax);
+    ``PREC_F32`` does with the oracle's f64 arithmetic on CUDA cores; the
+    default is the fused bf16 tcgen05 kernel (1e-2)."""
     L = lib()
     if not hasattr(L, "mimw_b200_oracle_attention"):
         raise MimwError(ERR_UNSUPPORTED, "attention not built")

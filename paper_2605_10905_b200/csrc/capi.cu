@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/mimw_b200.h"
+#include "attention_x3.h"
 #include "convert.h"
 #include "pool.h"
 #include "host_stage.h"
@@ -498,6 +499,38 @@ void host_attention_f32(const float *const *inputs, int n_inputs, float *o, floa
   check_cuda(cudaStreamSynchronize(s), "attention f32 execution");
 }
 
+// oracle_attention (oracles.cpp:119-145) at MIMW_PREC_F32_BF16X3: split-bf16 x3
+// on the tcgen05 GEMM (attention_x3.cu), one head at a time.
+void host_attention_x3(const float *q, const float *k, const float *v, float *o, float *lse, int64_t heads,
+                       int64_t seq, int64_t d, int64_t w, double scale) {
+  cudaStream_t s = cudaStreamPerThread;
+  const int64_t n = seq * d;
+  DevBuf din(sizeof(float) * (4 * n + seq), s);
+  DevBuf dws(mimw::attention_x3_workspace_bytes(seq, d), s);
+  float *f = din.as<float>();
+  for (int64_t h = 0; h < heads; ++h) {
+    const float *src[3] = {q + h * n, k + h * n, v + h * n};
+    for (int t = 0; t < 3; ++t)
+      check_cuda(cudaMemcpyAsync(f + t * n, src[t], sizeof(float) * n, cudaMemcpyHostToDevice, s), "H2D");
+    mimw::AttnX3Args a{};
+    a.q = f;
+    a.k = f + n;
+    a.v = f + 2 * n;
+    a.o = f + 3 * n;
+    a.lse = f + 4 * n;
+    a.seq = seq;
+    a.d = d;
+    a.w = w;
+    a.scale = scale;
+    a.workspace = dws.p;
+    check_cuda(mimw::attention_x3_launch(a, s), "attention x3 launch");
+    check_cuda(cudaMemcpyAsync(o + h * n, a.o, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H o");
+    if (lse)
+      check_cuda(cudaMemcpyAsync(lse + h * seq, a.lse, sizeof(float) * seq, cudaMemcpyDeviceToHost, s), "D2H lse");
+    check_cuda(cudaStreamSynchronize(s), "attention x3 execution");  // the next head reuses f
+  }
+}
+
 // oracle_attention (oracles.cpp:119-145) for `heads` independent [seq, d]
 // heads of host f32 Tiles stored back to back ([heads, seq, d]); heads == 1
 // is exactly the reference signature.  Head dim zero-padded to 128 (exact:
@@ -512,8 +545,8 @@ void host_attention_f32(const float *const *inputs, int n_inputs, float *o, floa
 void host_attention_heads(const float *q, const float *k, const float *v, float *o, float *lse,
                           int64_t heads, int64_t seq, int64_t d, int64_t w, double scale,
                           int precision = MIMW_PREC_BF16) {
-  require(precision == MIMW_PREC_BF16 || precision == MIMW_PREC_F32, MIMW_ERR_ARG,
-          "precision must be MIMW_PREC_BF16 or MIMW_PREC_F32");
+  require(precision == MIMW_PREC_BF16 || precision == MIMW_PREC_F32 || precision == MIMW_PREC_F32_BF16X3,
+          MIMW_ERR_ARG, "precision must be MIMW_PREC_BF16, MIMW_PREC_F32 or MIMW_PREC_F32_BF16X3");
   require(heads >= 0 && seq >= 0 && d >= 0, MIMW_ERR_SHAPE, "negative extent");
   require(d <= 128, MIMW_ERR_UNSUPPORTED, "head dim > 128 not supported");
   require(w >= 1 || seq == 0 || heads == 0, MIMW_ERR_ARG, "window must be >= 1");
@@ -533,6 +566,10 @@ void host_attention_heads(const float *q, const float *k, const float *v, float 
       const float *in[3] = {q + h * seq * d, k + h * seq * d, v + h * seq * d};
       host_attention_f32(in, 3, o + h * seq * d, lse ? lse + h * seq : nullptr, seq, d, w, 1, false, scale);
     }
+    return;
+  }
+  if (precision == MIMW_PREC_F32_BF16X3) {
+    host_attention_x3(q, k, v, o, lse, heads, seq, d, w, scale);
     return;
   }
   cudaStream_t s = cudaStreamPerThread, cs = side_stream(0), ds = side_stream(1);

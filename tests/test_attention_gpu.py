@@ -144,3 +144,54 @@ def test_reference_precision_attention_case(P, golden, w):
         got = P.run_oracle("attention", {"q": q, "k": k, "v": v}, {"w": 16, "scale": 0.25},
                            precision=P.PREC_F32)["o"]
         assert oracle.rel_error(got, case_outputs(case)["o"]) <= case["tolerance"]
+
+
+@pytest.mark.parametrize("w", [16, 5, 32])
+def test_x3_precision_attention_case(P, golden, w):
+    """MIMW_PREC_F32_BF16X3 (split-bf16 x3 on the tcgen05 GEMM, the drop-in
+    binding's attention path) holds the reference's own 1e-4
+    (acceptance.cpp:333-355) against the reference-generated golden output,
+    and matches the restated oracle at other windows."""
+    case = golden["attention_degeneration"]
+    xs = case_inputs(case)
+    q, k, v = xs["q"], xs["k2"], xs["v2"]
+    o, lse = P.oracle_attention(q, k, v, w, 0.25, with_lse=True, precision=P.PREC_F32_BF16X3)
+    want, wl = oracle.oracle_attention(q, k, v, w, 0.25, with_lse=True)
+    assert oracle.rel_error(o, want) <= 1e-4
+    assert np.abs(lse - wl).max() <= 1e-4
+    if w == 16:
+        assert oracle.rel_error(o, case_outputs(case)["o"]) <= case["tolerance"]  # 1e-4
+
+
+@pytest.mark.parametrize("s,d,w", [(1, 8, 1), (7, 3, 4), (33, 20, 1000), (300, 64, 17), (513, 128, 513),
+                                   (1000, 100, 64), (2048, 128, 300), (3000, 72, 2999), (5000, 64, 700)])
+def test_x3_attention_vs_oracle(P, s, d, w):
+    """x3 path vs the f64 oracle on ragged S / D, windows of 1, < S, = S and
+    > S; S = 3000 and 5000 run as 2 and 4 query-row blocks (64 MiB S + P per
+    block), the latter with each block's key range starting inside the
+    sequence (klo > 0)."""
+    rng = np.random.default_rng(s * 7 + d)
+    q, k, v = (rng.standard_normal((s, d)).astype(np.float32) for _ in range(3))
+    scale = 1.0 / np.sqrt(d)
+    o, lse = P.oracle_attention(q, k, v, w, scale, with_lse=True, precision=P.PREC_F32_BF16X3)
+    if s <= 1000:
+        want, wl = oracle.oracle_attention(q, k, v, w, scale, with_lse=True)
+        assert oracle.rel_error(o, want) <= 1e-4
+        assert np.abs(lse - wl).max() <= 1e-4
+    else:  # sampled rows incl. the first / last of each 256-row block
+        rows = sorted({0, 1, 255, 256, s // 2, s - 257, s - 1} | set(range(0, s, 397)))
+        for r in rows:
+            want, wl = oracle.oracle_attention_rows(q, k, v, w, scale, r, r + 1)
+            assert oracle.rel_error(o[r:r + 1], want) <= 1e-4, r
+            assert abs(float(lse[r]) - float(wl[0])) <= 1e-4 * max(1.0, abs(float(wl[0]))), r
+
+
+def test_x3_attention_heads(P):
+    """Several heads through the batched host entry (one workspace reused)."""
+    rng = np.random.default_rng(3)
+    h, s, d = 3, 200, 40
+    q, k, v = (rng.standard_normal((h, s, d)).astype(np.float32) for _ in range(3))
+    o = P.oracle_attention_heads(q, k, v, 50, 0.3, precision=P.PREC_F32_BF16X3)
+    for i in range(h):
+        want = oracle.oracle_attention(q[i], k[i], v[i], 50, 0.3)
+        assert oracle.rel_error(o[i], want) <= 1e-4, i

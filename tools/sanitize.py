@@ -50,5 +50,11 @@ sa_ = [torch.randn(300, kk, device="cuda").bfloat16() for kk in (64, 136, 0)]
 sb_ = [torch.randn(kk, 264, device="cuda").bfloat16() for kk in (64, 136, 0)]
 for cp in (-1, 1):
     MD.emulated_multi_device_gemm(sa_, sb_, comm_pairs=cp)
+# reference-precision host entries: split-bf16 x3 attention (GEMM + softmax split kernels)
+# and the f64 CUDA-core path, ragged S / D, window < S
+rng = np.random.default_rng(0)
+hq, hk, hv = (rng.standard_normal((75, 20)).astype(np.float32) for _ in range(3))
+P.oracle_attention(hq, hk, hv, 9, 0.3, precision=P.PREC_F32_BF16X3)
+P.oracle_attention(hq, hk, hv, 9, 0.3, precision=P.PREC_F32)
 torch.cuda.synchronize()
 print("sanitize run ok")

@@ -336,8 +336,24 @@ def gemm_mxfp8(a, sfa, b, sfb, out=None, stream=None, cta_group: int = 2):
     """Block-scaled FP8 GEMM: a e4m3 [M,K], sfa uint8 (UE8M0) [M,K/32],
     b e4m3 [N,K], sfb [N,K/32]  ->  bf16 [M,N] = (a*2^(sfa-127)) . (b*2^(sfb-127))^T."""
     import torch
+    f8 = (torch.float8_e4m3fn, torch.uint8)
+    for t, nm in ((a, "a"), (b, "b")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype not in f8 or t.dim() != 2:
+            raise MimwError(ERR_ARG, f"gemm_mxfp8 {nm}: expected a 2-D e4m3 (or uint8) CUDA tensor")
     m, k = a.shape
     n = b.shape[0]
+    if b.shape[1] != k:
+        raise MimwError(ERR_SHAPE, f"dot conformance: a.shape[1]={k} != b.shape[1]={b.shape[1]}")
+    for t, rows, nm in ((sfa, m, "sfa"), (sfb, n, "sfb")):
+        _need(t, torch.uint8, f"gemm_mxfp8 {nm}", 2)
+        if tuple(t.shape) != (rows, k // 32):
+            raise MimwError(ERR_SHAPE, f"gemm_mxfp8 {nm}: need uint8 [{rows}, {k // 32}] (one UE8M0 per 32 K)")
+    for t in (a, b, sfa, sfb):
+        if not t.is_contiguous() or t.device != a.device:
+            raise MimwError(ERR_UNSUPPORTED, "gemm_mxfp8 needs contiguous tensors on one device")
+    if out is not None and (tuple(out.shape) != (m, n) or out.dtype != torch.bfloat16
+                            or not out.is_contiguous() or out.device != a.device):
+        raise MimwError(ERR_SHAPE, f"gemm_mxfp8 out: need a contiguous bf16 [{m}, {n}] tensor")
     if out is None:
         out = torch.empty((m, n), device=a.device, dtype=torch.bfloat16)
     _check(lib().mimw_b200_gemm_mxfp8_ex(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), sfb.data_ptr(),
@@ -354,6 +370,10 @@ def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, c
     columns per CTA-pair tile (0 auto, 256, 512); ``swap_tails``: groups'
     < 256-row tails as swapped-operand tiles (None: the tile's default)."""
     import torch
+    _need(x, torch.bfloat16, "grouped_gemm x", 2)
+    _need(w, torch.bfloat16, "grouped_gemm w", 3)
+    if w.device != x.device:
+        raise MimwError(ERR_ARG, "grouped_gemm: x and w on different devices")
     offs = np.ascontiguousarray(np.asarray(m_offsets, dtype=np.int64))
     g = w.shape[0]
     if offs.shape != (g + 1,):
@@ -366,6 +386,9 @@ def grouped_gemm(x, m_offsets, w, out=None, w_layout: int = B_KN, stream=None, c
     for t in (x, w):
         if not t.is_contiguous():
             raise MimwError(ERR_UNSUPPORTED, "grouped_gemm needs contiguous tensors")
+    if out is not None and (out.dtype != torch.bfloat16 or out.dim() != 2 or out.shape[1] != n
+                            or out.shape[0] < offs[-1] or not out.is_contiguous() or out.device != x.device):
+        raise MimwError(ERR_SHAPE, f"grouped_gemm out: need a contiguous bf16 [>= {int(offs[-1])}, {n}] tensor")
     if out is None:
         out = torch.empty((x.shape[0], n), device=x.device, dtype=torch.bfloat16)
     _check(lib().mimw_b200_grouped_gemm_bf16_ex(x.data_ptr(), offs.ctypes.data, w.data_ptr(),
@@ -405,12 +428,18 @@ def simplicial_attention_fwd(q, k1, v1, k2, v2, w1: int, w2: int, scale: float |
                              out=None, lse=None, want_lse: bool = True, stream=None):
     """2-simplicial attention forward on bf16 CUDA tensors [BH, S, 128]."""
     import torch
+    for t, nm in ((q, "q"), (k1, "k1"), (v1, "v1"), (k2, "k2"), (v2, "v2")):
+        _need(t, torch.bfloat16, f"simplicial_attention_fwd {nm}", 3)
     bh, s, d = q.shape
     if d != 128:
         raise MimwError(ERR_UNSUPPORTED, "device simplicial attention supports head_dim == 128")
     for t in (q, k1, v1, k2, v2):
-        if not t.is_contiguous() or t.shape != q.shape:
+        if not t.is_contiguous() or t.shape != q.shape or t.device != q.device:
             raise MimwError(ERR_UNSUPPORTED, "contiguous [BH, S, 128] tensors of one shape required")
+    if out is not None and (out.shape != q.shape or out.dtype != torch.bfloat16 or not out.is_contiguous()):
+        raise MimwError(ERR_SHAPE, "simplicial_attention_fwd out: need a contiguous bf16 tensor of q's shape")
+    if lse is not None and (tuple(lse.shape) != (bh, s) or lse.dtype != torch.float32 or not lse.is_contiguous()):
+        raise MimwError(ERR_SHAPE, "simplicial_attention_fwd lse: need a contiguous f32 [BH, S] tensor")
     if out is None:
         out = torch.empty_like(q)
     if lse is None and want_lse:
@@ -429,12 +458,22 @@ def attention_bwd(q, k, v, o, do, lse, window: int | None = None, scale: float |
     given the forward's output ``o`` and ``lse`` (fp32 [B, H, S]) and the
     upstream gradient ``do``.  ``causal=False`` for non-causal attention."""
     import torch
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (do, "do")):
+        _need(t, torch.bfloat16, f"attention_bwd {nm}", 4)
+        if t.shape != q.shape:
+            raise MimwError(ERR_SHAPE, f"attention_bwd {nm}: shape {tuple(t.shape)} != q's {tuple(q.shape)}")
     b, h, s, d = q.shape
+    _need(lse, torch.float32, "attention_bwd lse", 3)
+    if tuple(lse.shape) != (b, h, s):
+        raise MimwError(ERR_SHAPE, f"attention_bwd lse: need f32 [{b}, {h}, {s}]")
+    for t, nm in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        if t is not None and (t.shape != q.shape or t.dtype != torch.bfloat16 or not t.is_contiguous()):
+            raise MimwError(ERR_SHAPE, f"attention_bwd {nm}: need a contiguous bf16 tensor of q's shape")
     if d != 128:
         raise MimwError(ERR_UNSUPPORTED, "device attention supports head_dim == 128")
     for t in (q, k, v, o, do, lse):
-        if not t.is_contiguous():
-            raise MimwError(ERR_UNSUPPORTED, "attention_bwd needs contiguous tensors")
+        if not t.is_contiguous() or t.device != q.device:
+            raise MimwError(ERR_UNSUPPORTED, "attention_bwd needs contiguous tensors on one device")
     if scale is None:
         scale = d ** -0.5
     if not causal:

@@ -129,6 +129,48 @@ def test_wrapper_validation(P):
     assert r == P.ERR_SHAPE or r == P.ERR_UNSUPPORTED
 
 
+def test_wrapper_validation_other_kernels(P):
+    """gemm_mxfp8, grouped_gemm, simplicial_attention_fwd and attention_bwd
+    reject mis-typed / mis-shaped operands before any launch (the C side
+    builds its tensor maps from one operand's extents)."""
+    import torch
+    cu = dict(device="cuda")
+    qa = torch.zeros((128, 256), dtype=torch.uint8, **cu).view(torch.float8_e4m3fn)
+    sf = torch.zeros((128, 8), dtype=torch.uint8, **cu)
+    P.gemm_mxfp8(qa, sf, qa, sf)  # well-formed
+    bad = [
+        lambda: P.gemm_mxfp8(qa, sf[:, :4].contiguous(), qa, sf),                 # sfa too small
+        lambda: P.gemm_mxfp8(qa, sf, qa[:, :128].contiguous(), sf),               # K mismatch
+        lambda: P.gemm_mxfp8(qa.view(torch.uint8).bfloat16(), sf, qa, sf),        # dtype
+    ]
+    x = torch.zeros((40, 64), dtype=torch.bfloat16, **cu)
+    w = torch.zeros((2, 64, 96), dtype=torch.bfloat16, **cu)
+    P.grouped_gemm(x, [0, 10, 40], w)
+    bad += [
+        lambda: P.grouped_gemm(x.float(), [0, 10, 40], w),                        # dtype
+        lambda: P.grouped_gemm(x, [0, 10, 40], w[:, :32].contiguous()),           # K mismatch
+        lambda: P.grouped_gemm(x, [0, 10, 40], w, out=torch.zeros((40, 64), dtype=torch.bfloat16, **cu)),
+    ]
+    t = torch.zeros((1, 64, 128), dtype=torch.bfloat16, **cu)
+    P.simplicial_attention_fwd(t, t, t, t, t, 2, 16)
+    bad += [
+        lambda: P.simplicial_attention_fwd(t, t, t.float(), t, t, 2, 16),         # dtype
+        lambda: P.simplicial_attention_fwd(t, t, t, t[:, :32].contiguous(), t, 2, 16),  # shape
+    ]
+    q = torch.zeros((1, 1, 64, 128), dtype=torch.bfloat16, **cu)
+    lse = torch.zeros((1, 1, 64), **cu)
+    P.attention_bwd(q, q, q, q, q, lse)
+    bad += [
+        lambda: P.attention_bwd(q, q, q, q, q, lse[:, :, :32].contiguous()),      # lse shape
+        lambda: P.attention_bwd(q, q[:, :, :32].contiguous(), q, q, q, lse),      # k shape
+        lambda: P.attention_bwd(q, q, q, q, q.float(), lse),                      # dtype
+    ]
+    for i, f in enumerate(bad):
+        with pytest.raises(P.MimwError):
+            f()
+    torch.cuda.synchronize()
+
+
 def test_run_oracle_simplicial_defaults(P):
     """run_oracle uses the reference's scalar defaults sc("w1", 2), sc("w2", 16),
     sc("scale", 1.0) (oracles.cpp:190-193)."""

@@ -73,6 +73,35 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
     return LIB
 
 
+def build_mutant(tag: int, out_dir: str, clc_slots: int = 4, perturb: int = 1) -> str:
+    """Test build for tests/test_mutation_gpu.py (the GPU form of the reference's
+    barrier-deletion test, acceptance.cpp:461-485): gemm_bf16.cu recompiled with
+    the wide GEMM's mbarrier wait `tag` deleted (-DMIMW_MUTATE_WAIT, gemm_wide.cuh;
+    0 deletes nothing: the control), schedule perturbation `perturb` (0: off),
+    `clc_slots` tile-id ring slots and a ~1 s watchdog, linked with the product
+    objects into out_dir.  Never loaded by the package itself."""
+    build()
+    os.makedirs(out_dir, exist_ok=True)
+    src = os.path.join(CSRC, "gemm_bf16.cu")
+    name = f"mut{tag}_s{clc_slots}_p{perturb}"
+    obj = os.path.join(out_dir, f"gemm_bf16_{name}.o")
+    lib = os.path.join(out_dir, f"libmimw_{name}.so")
+    flags = [f for f in FLAGS if f != "-v" and f != "-Xptxas"]
+    defs = [f"-DMIMW_MUTATE_WAIT={tag}", f"-DMIMW_CLC_SLOTS={clc_slots}", "-DMIMW_WATCHDOG_CYCLES=(1ull<<31)"]
+    if perturb:
+        defs.append(f"-DMIMW_PERTURB={perturb}")
+    cmd = [NVCC] + flags + defs + ["-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for mutant {tag}:\n{r.stderr[-4000:]}")
+    objs = [o for o in sorted(glob.glob(os.path.join(BUILD, "*.o"))) if not o.endswith("gemm_bf16.o")]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", lib, obj] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed for mutant {tag}:\n{r.stderr[-4000:]}")
+    return lib
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")

@@ -23,6 +23,41 @@
 // 4-stage ring of 48 KiB (A 16 KiB + B 2 x 16 KiB).  Tiles by cluster
 // launch control, as the narrow kernel (gemm_clc.mimw:1-34).
 
+// Mutation testing (tests/test_mutation_gpu.py, the GPU form of the reference's
+// barrier-deletion test, acceptance.cpp:461-485): a test build with
+// -DMIMW_MUTATE_WAIT=t deletes this kernel's mbarrier wait tagged t (the tag
+// is also the watchdog tag of that wait).  Product builds leave it 0.
+#ifndef MIMW_MUTATE_WAIT
+#define MIMW_MUTATE_WAIT 0
+#endif
+#define WIDE_WAIT(tag, ...)                          \
+  do {                                               \
+    if constexpr (MIMW_MUTATE_WAIT != (tag)) __VA_ARGS__; \
+  } while (0)
+
+// Schedule perturbation for the mutation test (the GPU stand-in for the
+// reference simulator's SeededRandom scheduler, sim.cpp:252-316): a test build
+// with -DMIMW_PERTURB=seed sleeps 0.5-16.5 us at a quarter of the visits of two
+// sites (epilogue before draining a tile; the CLC issuer before a request), so
+// the roles drift against each other far more than on an undisturbed run.
+#ifdef MIMW_PERTURB
+__device__ __forceinline__ void wide_perturb(uint32_t site, uint32_t t) {
+  uint32_t h = site * 0x9E3779B9u ^ (t + 1u) * 0x85EBCA6Bu ^ (uint32_t)(MIMW_PERTURB)*0xC2B2AE35u ^
+               (blockIdx.x + 1u) * 0x27D4EB2Fu ^ (threadIdx.x >> 5) * 0x165667B1u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  if ((h & 3) == 0) __nanosleep(500 + (h >> 8) % 16000);
+}
+#else
+__device__ __forceinline__ void wide_perturb(uint32_t, uint32_t) {}
+#endif
+#ifndef MIMW_CLC_SLOTS
+#define MIMW_CLC_SLOTS 4  // tile-id response ring (the mutation test also builds it with 2)
+#endif
+
 constexpr int WIDE_BN = 512;               // C columns per pair tile
 constexpr int WIDE_NB_CTA = 256;           // B columns staged per CTA (two halves of 128)
 constexpr int WIDE_EPI_WARPS = 8;
@@ -96,7 +131,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t tfull_bar = bar_base + 8 * (2 * WIDE_STAGES);
   const uint32_t tempty_bar = tfull_bar + 8;
   const uint32_t tmem_slot = tempty_bar + 8;
-  constexpr int CLC_SLOTS = 4;
+  constexpr int CLC_SLOTS = MIMW_CLC_SLOTS;
   constexpr uint32_t CLC_CONSUMERS = 2 * (1 + WIDE_EPI_WARPS) + 1;
   auto clc_resp = [&](int s) { return bar_base + 128 + 16 * s; };
   auto clc_full = [&](int s) { return bar_base + 128 + 16 * CLC_SLOTS + 8 * s; };
@@ -141,7 +176,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   auto next_tile = [&](int t, int u, bool arrive) -> int {
     if (!clc) return t + nclusters;
     const int slot = u % CLC_SLOTS;
-    mbar_wait(clc_full(slot), (uint32_t)(u / CLC_SLOTS) & 1, 12);
+    WIDE_WAIT(12, mbar_wait(clc_full(slot), (uint32_t)(u / CLC_SLOTS) & 1, 12));
     const int x = clc_query(clc_resp(slot));
     if (arrive) mbar_arrive_cluster(map_to_rank(clc_empty(slot), 0));
     return x < 0 ? num_tiles : x / 2;
@@ -149,7 +184,8 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   auto clc_request = [&](int u) {
     const int slot = u % CLC_SLOTS;
     if (crank == 0) {
-      mbar_wait_cluster(clc_empty(slot), ((uint32_t)(u / CLC_SLOTS) & 1) ^ 1, 13);
+      wide_perturb(2, (uint32_t)u);
+      WIDE_WAIT(13, mbar_wait_cluster(clc_empty(slot), ((uint32_t)(u / CLC_SLOTS) & 1) ^ 1, 13));
       mbar_arrive_expect_tx(clc_full(slot), 16);
       clc_try_cancel_multicast(clc_resp(slot), clc_full(slot));
     } else {
@@ -171,7 +207,7 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int m0 = tc.row_base + tc.mt * 256 + (int)rank * (tc.swap_n ? tc.swap_n / 2 : BM_CTA);
         const int n0 = tc.nt * WIDE_BN + (int)rank * 128;
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1);
+          WIDE_WAIT(1, mbar_wait_cluster(empty_bar(stage), phase ^ 1, 1));
           const uint32_t fb = full_target0 + 8 * stage;
           // swapped tail: only the tail's swap_n / 2 X rows per CTA (16-row boxes), not a 128-row box
           const int xrows = GROUPED && tc.swap_n ? tc.swap_n / 2 : BM_CTA;
@@ -220,11 +256,11 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if constexpr (GROUPED) swap_n = sched.decode(t).swap_n;
         // swapped: A = W^T (the B slot; MN-major for [G,K,N]), B = the tail's X rows (the A slot)
         const uint32_t idesc = swap_n ? idesc_bf16(256, swap_n, B_MN ? 1 : 0, 0) : IDESC;
-        mbar_wait_cluster(tempty_bar, acc_phase ^ 1, 2);
+        WIDE_WAIT(2, mbar_wait_cluster(tempty_bar, acc_phase ^ 1, 2));
         tc_fence_after();
         if (lane_id() == 0) TILE_TRACE(t, 0, gtimer());
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(full_bar(stage), phase, 3);
+          WIDE_WAIT(3, mbar_wait(full_bar(stage), phase, 3));
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sa = sbase + stage * WIDE_STAGE_BYTES;
@@ -266,9 +302,10 @@ gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const TileCoord tc = sched.decode(t);
       const int row0 = tc.mt * 256 + (int)rank * BM_CTA + q * 32;
       const int col0 = tc.nt * WIDE_BN + half * 256;
-      mbar_wait(tfull_bar, acc_phase, 4);
+      WIDE_WAIT(4, mbar_wait(tfull_bar, acc_phase, 4));
       acc_phase ^= 1;
       tc_fence_after();
+      wide_perturb(1, (uint32_t)t);
 #ifdef MIMW_TILE_TRACE
       if (warp == 2 && leader && lane == 0) TILE_TRACE(t, 2, gtimer());
 #endif

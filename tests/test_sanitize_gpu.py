@@ -23,9 +23,15 @@ def _run(tool):
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(exe):
         pytest.skip("compute-sanitizer not available")
+    if "/graft/" in os.path.realpath(exe):
+        # The GPU pool replaces compute-sanitizer with a refusing stub (runs under it left
+        # GPUs needing a reset); the same kernels' bounds are covered by the parity suites.
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     r = subprocess.run([exe, "--tool", tool, "--print-limit", "50", sys.executable,
                         os.path.join(ROOT, "tools", "sanitize.py")],
                        capture_output=True, text=True, timeout=600)
+    if "closed on this pool" in r.stdout + r.stderr:
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     assert "sanitize run ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
     return r.stdout + r.stderr
 

@@ -289,7 +289,7 @@ def reassembly_ms(fn, ws, reps=5):
 # ---------------------------------------------------------------------------
 # CPU reference path (oracle/_ref = the unmodified reference oracles)
 # ---------------------------------------------------------------------------
-def cpu_gemm_sample(seconds_target: float = 12.0):
+def cpu_gemm_sample(seconds_target: float = 12.0, single: bool = True):
     """Time oracle_gemm (oracles.cpp:14-26) on a row sample of the 8192^3
     workload with all host threads (one row block each), plus the as-shipped
     single-thread rate on a 2-row sample; returns a cpu_baseline dict."""
@@ -322,7 +322,7 @@ def cpu_gemm_sample(seconds_target: float = 12.0):
         dt = run(rows, threads)
     flops = 2.0 * rows * GEMM_N * GEMM_K
     one = None
-    if R is not None and threads > 1:
+    if R is not None and threads > 1 and single:
         dt1 = run(2, 1)
         one = 2.0 * 2 * GEMM_N * GEMM_K / dt1 / 1e12
     return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": threads, "kind": kind,
@@ -1023,17 +1023,21 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
+        # every warm-up and timed step is one bounded row sample, sized so the
+        # whole --steps K --warmup W run stays near 2 minutes
+        per = min(12.0, max(1.0, 120.0 / (args.steps + args.warmup)))
+        for _ in range(args.warmup):
+            cpu_gemm_sample(per, single=False)
         vals, info = [], None
-        for _ in range(max(1, args.steps)):
-            info = cpu_gemm_sample()
-            vals.append(info["value"])
-            if len(vals) >= 3:  # each step is a bounded sample; keep the run to minutes
-                break
+        for st in range(max(1, args.steps)):
+            r = cpu_gemm_sample(per, single=(st == 0))
+            info = info or r
+            vals.append(r["value"])
         v = float(np.median(vals))
         fa = cpu_attention_sample()
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS",
                "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": len(vals),
-               "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                "dtype": "f32", "data": "synthetic U[-1,1] rounded to bf16",
                "config": {"workload": "configs[1] GEMM 8192^3 via reference oracle_gemm "
                                       "(oracles.cpp:14-26) on host cores, row-sampled"},
